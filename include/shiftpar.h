@@ -1,0 +1,153 @@
+/*
+ * shiftpar.h — C-ABI of the B200 (sm_100a) Shift-Parallel forward path.
+ *
+ * The drop-in boundary between the Python engine (paper_2507_11830_b200,
+ * mirroring the reference `shiftsim` Engine API) and the hand-written CUDA
+ * kernels in libshiftpar.so.  Conventions:
+ *   - plain pointers to caller-owned DEVICE memory, sizes in elements,
+ *     row strides ("ld") in elements; no torch types;
+ *   - every call is stream-ordered on `stream` (a cudaStream_t, passed as
+ *     void*), never synchronises, never allocates device memory;
+ *   - return 0 on success, a nonzero sp_status otherwise; sp_last_error()
+ *     returns the message of the last failure on the calling thread.
+ *     The Python wrapper maps nonzero codes to ContractViolation
+ *     (reference errors.py:4-13) BEFORE any further work is enqueued.
+ *
+ * Each entry cites the reference interface it replaces
+ * (/root/reference/pkg/src/shiftsim/<file>:<line>).
+ */
+#ifndef SHIFTPAR_H_
+#define SHIFTPAR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int sp_status;
+#define SP_OK 0
+#define SP_ERR_INVALID 1     /* argument outside the contract (-> ContractViolation) */
+#define SP_ERR_CUDA 2        /* CUDA runtime/launch error */
+#define SP_ERR_UNSUPPORTED 3 /* shape/arch the kernels do not cover */
+
+/* GEMM epilogues (sp_gemm_bf16 `epilogue`) */
+#define SP_EPI_STORE_BF16 0 /* D(bf16)  = acc */
+#define SP_EPI_STORE_F32 1  /* D(f32)   = acc */
+#define SP_EPI_ADD_F32 2    /* D(f32)  += acc (residual stream, in place) */
+#define SP_EPI_SWIGLU 3     /* D(bf16)  = silu(acc[:, gate]) * acc[:, up]; B rows interleaved
+                               in 128-row chunks [gate 128 | up 128], D width N/2 */
+#define SP_EPI_GELU 4       /* D(bf16)  = gelu_tanh(acc) (reference-compat MLP) */
+
+/* -------------------------------------------------------------- runtime */
+const char* sp_last_error(void);
+int sp_abi_version(void);
+/* 0 when the current device is sm_100 (B200) and the kernels can run. */
+sp_status sp_device_check(int* sm_count);
+
+/* --------------------------------------------------------------- GEMM
+ * Replaces tensor_core.matmul (tensor_core.py:75-102) for every projection:
+ * QKV (parallel_engine.py:359-361 / :479-481), O (:369 / :515), MLP
+ * (:374-377 / :516-517) and the LM head (:394 / :534).
+ *
+ *   D[m, n] = epi( sum_k A[m, k] * B[n, k] )        (bf16 in, f32 accumulate)
+ *
+ * A: logical [M, K] bf16.  If a_kchunk > 0, K is stored as K/a_kchunk
+ *    chunks: element (m, k) lives at A + (k / a_kchunk) * a_chunk_stride
+ *    + m * lda + (k % a_kchunk)  (the per-peer layout an all-to-all receive
+ *    leaves behind — SP head->seq unpack fused into the operand load).
+ * B: [N, K] bf16 (nn.Linear layout, K contiguous), row stride ldb; a TP shard
+ *    is a row range or a K-column window of the resident replica (zero copy).
+ * D: row stride ldd.  If peer_width > 0, column n is written to
+ *    D + (n / peer_width) * peer_stride + m * ldd + (n % peer_width)
+ *    (the per-peer contiguous send layout of the SP seq->head all-to-all,
+ *    i.e. the pack fused into the epilogue).
+ * Fixed tiling, no split-K: each D element is one ascending-K reduction
+ * independent of M and of the N window -> row/column splits are bit-exact
+ * (the property of tensor_core.py:1-28 the SP path relies on).
+ */
+sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_chunk_stride,
+                       const void* B, int64_t ldb, void* D, int64_t ldd, int M, int N, int K,
+                       int epilogue, int64_t peer_width, int64_t peer_stride, void* stream);
+
+/* ------------------------------------------------ embedding / norms
+ * Embedding gather (parallel_engine.py:339-346 TP, :462-469 SP): out[r, :] =
+ * f32(table[ids[r], :]) (+ pos_table[pos[r], :] when pos_table != NULL, the
+ * reference's additive sinusoidal rows, tensor_core.py:184-206).
+ */
+sp_status sp_embed(const int32_t* ids, const void* table_bf16, const int32_t* pos,
+                   const float* pos_table, float* out_f32, int rows, int hidden, void* stream);
+
+/* Fused residual-add + RMSNorm (tensor_core.py:115-123 at parallel_engine.py
+ * :354,:372,:390,:477,:516,:533):
+ *   if add != NULL: x[r] += add[r]   (written back — the TP all-reduce result)
+ *   out[r] = bf16( gain * x[r] / sqrt(mean(x[r]^2) + eps) )
+ * If row_idx != NULL, input row r is x[row_idx[r]] (final norm on end rows).
+ */
+sp_status sp_add_rmsnorm(float* x, int64_t ldx, const float* add, const float* gain, float eps,
+                         const int32_t* row_idx, void* out_bf16, int64_t ldo, int rows,
+                         int hidden, void* stream);
+
+/* ----------------------------------------------- RoPE + paged KV write
+ * Replaces KvCache.append (kv_cache.py:99-122) plus positions: for each
+ * token r of qkv ([rows, q_heads+2*kv_heads, head_dim] at row stride ldqkv,
+ * layout [q | k | v]) apply rotate-half RoPE (table [max_pos, d/2, 2] f32;
+ * NULL = no rotation) at pos[r] to q and k, write rotated q to q_out
+ * (NULL or q_heads == 0 -> skipped) and k/v to the head-sharded paged pool
+ * ([num_blocks][kv_heads][block_size][head_dim], this layer's slice) at
+ * slot[r] (block = slot / block_size); slot < 0 skips the row.
+ */
+sp_status sp_rope_kv_write(const void* qkv, int64_t ldqkv, const int32_t* pos,
+                           const int32_t* slot, const float* rope_table, void* q_out,
+                           int64_t ldq, void* k_pool, void* v_pool, int rows, int q_heads,
+                           int kv_heads, int head_dim, int block_size, void* stream);
+
+/* ----------------------------------------------------- paged attention
+ * Replaces attend_cached (tensor_core.py:135-176) looped per (item, head)
+ * at parallel_engine.py:362-368 (TP) / :494-500 (SP) / tails :423-429,
+ * :603-611.  Item i owns q rows [cu_q[i], cu_q[i+1]); its first query sits
+ * at absolute position first_pos[i] and may attend keys j <= first_pos[i]+t
+ * of a window of kv_len[i] keys read through block_tables row i.
+ * GQA: q head h reads kv head h / (q_heads / kv_heads).
+ * work: int32 pairs (item, first q row of a tile) — host-built schedule;
+ * pass n_work = 0 to let the call build the decode schedule (1 row/item).
+ * ws: f32 workspace of sp_attn_workspace_bytes() bytes (split-KV partials).
+ */
+sp_status sp_attention(const void* q, int64_t ldq, const void* k_pool, const void* v_pool,
+                       const int32_t* block_tables, int64_t bt_stride, const int32_t* cu_q,
+                       const int32_t* first_pos, const int32_t* kv_len, int n_items,
+                       const int32_t* work, int n_work, int max_q_len, int max_kv_len,
+                       void* out, int64_t ldo, int q_heads, int kv_heads, int head_dim,
+                       int block_size, void* ws, int64_t ws_bytes, void* stream);
+int64_t sp_attn_workspace_bytes(int n_items, int q_heads, int head_dim, int max_kv_len);
+/* Rows per prefill work tile for a (q_heads, kv_heads) pair (host schedule). */
+int sp_attn_tile_tokens(int q_heads, int kv_heads);
+
+/* ------------------------------------------- all-to-all pack / unpack
+ * The reference re-shards with np.ascontiguousarray(tensor[:, lo:hi, :])
+ * per peer (parallel_engine.py:539-542) and np.concatenate(..., axis=1)
+ * on receive (:514).  pack: src [rows, P*w] -> dst [P][rows][w];
+ * unpack: src [P][rows][w] -> dst [rows, P*w]  (bf16, w % 8 == 0).
+ */
+sp_status sp_a2a_pack(const void* src, int64_t lds, void* dst, int rows, int peers, int width,
+                      void* stream);
+sp_status sp_a2a_unpack(const void* src, void* dst, int64_t ldd, int rows, int peers,
+                        int width, void* stream);
+
+/* ---------------------------------------------- reductions and heads
+ * In-process (loopback) all-reduce: dst = a + b, f32, ascending order as in
+ * DeviceGroup.all_reduce_sum (fabric.py:117-143).
+ */
+sp_status sp_add_f32(const float* a, const float* b, float* dst, int64_t n, void* stream);
+/* greedy_token (model.py:303-307): per row argmax, lowest index wins ties. */
+sp_status sp_argmax(const float* logits, int64_t ld, int rows, int vocab, int32_t* idx,
+                    float* val, void* stream);
+/* dst[r, :] = src[idx[r], :] for f32 rows (end-row / tail selection). */
+sp_status sp_gather_rows_f32(const float* src, int64_t lds, const int32_t* idx, float* dst,
+                             int64_t ldd, int rows, int width, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SHIFTPAR_H_ */

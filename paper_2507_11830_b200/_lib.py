@@ -1,0 +1,74 @@
+"""ctypes binding of libshiftpar.so — the C-ABI declared in include/shiftpar.h.
+
+The library is built in-tree (``python -m paper_2507_11830_b200.build`` or
+``__graft_entry__.build()``) and loaded from the package directory.  There is
+no fallback: if the library is missing every op raises ``LibraryMissing``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import ContractViolation, LibraryMissing
+
+LIB_NAME = "libshiftpar.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+_c_int = ctypes.c_int
+_i64 = ctypes.c_int64
+_vp = ctypes.c_void_p
+_f32 = ctypes.c_float
+
+# name -> (restype, argtypes); must match include/shiftpar.h exactly
+SIGNATURES = {
+    "sp_last_error": (ctypes.c_char_p, []),
+    "sp_abi_version": (_c_int, []),
+    "sp_device_check": (_c_int, [ctypes.POINTER(_c_int)]),
+    "sp_gemm_bf16": (_c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _c_int, _c_int, _c_int,
+                              _c_int, _i64, _i64, _vp]),
+    "sp_embed": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _vp]),
+    "sp_add_rmsnorm": (_c_int, [_vp, _i64, _vp, _vp, _f32, _vp, _vp, _i64, _c_int, _c_int, _vp]),
+    "sp_rope_kv_write": (_c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _c_int, _c_int,
+                                  _c_int, _c_int, _c_int, _vp]),
+    "sp_attention": (_c_int, [_vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _c_int, _vp, _c_int,
+                              _c_int, _c_int, _vp, _i64, _c_int, _c_int, _c_int, _c_int, _vp, _i64,
+                              _vp]),
+    "sp_attn_workspace_bytes": (_i64, [_c_int, _c_int, _c_int, _c_int]),
+    "sp_attn_tile_tokens": (_c_int, [_c_int, _c_int]),
+    "sp_a2a_pack": (_c_int, [_vp, _i64, _vp, _c_int, _c_int, _c_int, _vp]),
+    "sp_a2a_unpack": (_c_int, [_vp, _vp, _i64, _c_int, _c_int, _c_int, _vp]),
+    "sp_add_f32": (_c_int, [_vp, _vp, _vp, _i64, _vp]),
+    "sp_argmax": (_c_int, [_vp, _i64, _c_int, _c_int, _vp, _vp, _vp]),
+    "sp_gather_rows_f32": (_c_int, [_vp, _i64, _vp, _vp, _i64, _c_int, _c_int, _vp]),
+}
+
+_lib = None
+
+
+def load():
+    """Load libshiftpar.so (once).  Raises LibraryMissing if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise LibraryMissing(
+            f"{LIB_PATH} not found: build it with `python -m paper_2507_11830_b200.build` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def exported_symbols():
+    return sorted(SIGNATURES)
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().sp_last_error().decode(errors="replace")
+        raise ContractViolation(f"{what} failed (status {rc}): {msg}")

@@ -1,0 +1,525 @@
+// Paged causal attention over the head-sharded KV pool (sm_100a).
+//
+// Replaces tensor_core.attend_cached (tensor_core.py:135-176) as looped per
+// (item, local head) by the reference engine (parallel_engine.py:362-368 TP,
+// :494-500 SP, SwiftKV tails :423-429 / :603-611).  Semantics: item i's query
+// row t sits at absolute position first_pos[i] + t and sees keys
+// j <= first_pos[i] + t of its kv_len[i]-key window; softmax in f32.
+//
+// Prefill kernel: GQA-packed rows — one CTA owns one kv head and a tile of
+// (64 / G) tokens x G query heads = 64 packed rows, so each K/V tile loaded
+// from the paged pool (cp.async, 128-byte XOR swizzle) feeds all G heads.
+// Q K^T and P V run on m16n8k16 bf16 MMAs with f32 online softmax in registers.
+// Decode kernel: one CTA per (item, kv head, split); each warp streams its own
+// key tiles (double-buffered) for the G packed heads; warps merge in smem and
+// splits merge in a combine kernel (flash-decoding).
+#include "../../include/shiftpar.h"
+#include "common.cuh"
+
+namespace sp {
+namespace attn {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+struct Params {
+  const __nv_bfloat16* q;
+  int64_t ldq;
+  const __nv_bfloat16* k_pool;
+  const __nv_bfloat16* v_pool;
+  const int32_t* block_tables;
+  int64_t bt_stride;
+  const int32_t* cu_q;
+  const int32_t* first_pos;
+  const int32_t* kv_len;
+  const int2* work;
+  __nv_bfloat16* out;
+  int64_t ldo;
+  int q_heads, kv_heads, group, block_size;
+  float scale_log2;
+  // decode split-KV
+  int n_splits;
+  float* ws_o;    // [items][q_heads][splits][HD]
+  float* ws_lse;  // [items][q_heads][splits]
+};
+
+// physical 16-byte chunk index of logical (row, chunk) in a [rows][HD] bf16 tile
+template <int HD>
+__device__ __forceinline__ int swz(int row, int c) {
+  constexpr int NCH = HD / 8;
+  if constexpr (NCH >= 8) {
+    return c ^ (row & 7);
+  } else {
+    return c ^ ((row >> 1) & 3);
+  }
+}
+
+template <int HD>
+__device__ __forceinline__ uint32_t tile_addr(const __nv_bfloat16* base, int row, int c) {
+  return smem_u32(base + row * HD + swz<HD>(row, c) * 8);
+}
+
+// async-load `rows` keys [k0, k0+rows) of one kv head into a swizzled tile
+template <int HD>
+__device__ __forceinline__ void load_kv_tile(__nv_bfloat16* sdst, const __nv_bfloat16* pool,
+                                             const int32_t* bt, int kvh, int kv_heads,
+                                             int block_size, int k0, int rows, int kv_len,
+                                             int tid, int nthreads) {
+  constexpr int NCH = HD / 8;
+  for (int i = tid; i < rows * NCH; i += nthreads) {
+    const int r = i / NCH, c = i % NCH;
+    const int j = k0 + r;
+    const bool ok = j < kv_len;
+    const __nv_bfloat16* src = pool;
+    if (ok) {
+      const int64_t page = bt[j / block_size];
+      src = pool + ((page * kv_heads + kvh) * block_size + (j % block_size)) * HD + c * 8;
+    }
+    cp_async16(sdst + r * HD + swz<HD>(r, c) * 8, src, ok);
+  }
+}
+
+// S[16 x KT] = Q[16 x HD] K^T for one warp; qf: Q fragments per k-step
+template <int HD, int KT>
+__device__ __forceinline__ void qk_tile(float (&s)[KT / 8][4], const uint32_t (&qf)[HD / 16][4],
+                                        const __nv_bfloat16* sK, int lane) {
+#pragma unroll
+  for (int j = 0; j < KT / 8; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < HD / 16; ++ks) {
+#pragma unroll
+    for (int j = 0; j < KT / 8; j += 2) {
+      const int m = lane >> 3;
+      const int key = (j + (m >> 1)) * 8 + (lane & 7);
+      uint32_t b0, b1, b2, b3;
+      ldmatrix_x4(tile_addr<HD>(sK, key, ks * 2 + (m & 1)), b0, b1, b2, b3);
+      mma_bf16_16816(s[j], qf[ks], b0, b1);
+      mma_bf16_16816(s[j + 1], qf[ks], b2, b3);
+    }
+  }
+}
+
+// O[16 x HD] += P[16 x KT] V[KT x HD]
+template <int HD, int KT>
+__device__ __forceinline__ void pv_tile(float (&o)[HD / 8][4], const float (&s)[KT / 8][4],
+                                        const __nv_bfloat16* sV, int lane) {
+#pragma unroll
+  for (int kk = 0; kk < KT / 16; ++kk) {
+    uint32_t a[4];
+    a[0] = pack_bf16x2(s[2 * kk][0], s[2 * kk][1]);
+    a[1] = pack_bf16x2(s[2 * kk][2], s[2 * kk][3]);
+    a[2] = pack_bf16x2(s[2 * kk + 1][0], s[2 * kk + 1][1]);
+    a[3] = pack_bf16x2(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+#pragma unroll
+    for (int n = 0; n < HD / 8; n += 2) {
+      const int m = lane >> 3;
+      const int key = kk * 16 + (m & 1) * 8 + (lane & 7);
+      uint32_t b0, b1, b2, b3;
+      ldmatrix_x4_trans(tile_addr<HD>(sV, key, n + (m >> 1)), b0, b1, b2, b3);
+      mma_bf16_16816(o[n], a, b0, b1);
+      mma_bf16_16816(o[n + 1], a, b2, b3);
+    }
+  }
+}
+
+// masked online-softmax update for the two rows a thread holds
+template <int HD, int KT>
+__device__ __forceinline__ void softmax_update(float (&s)[KT / 8][4], float (&o)[HD / 8][4],
+                                               float (&mrow)[2], float (&lrow)[2], int kbase,
+                                               const int (&limit)[2], bool need_mask,
+                                               float scale_log2, int lane) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < KT / 8; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        float v = s[j][2 * h + e] * scale_log2;
+        if (need_mask) {
+          const int key = kbase + j * 8 + (lane & 3) * 2 + e;
+          if (key > limit[h]) v = -INFINITY;
+        }
+        s[j][2 * h + e] = v;
+        mx = fmaxf(mx, v);
+      }
+    }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float mnew = fmaxf(mrow[h], mx);
+    const float msafe = mnew == -INFINITY ? 0.f : mnew;
+    const float corr = exp2f(mrow[h] - msafe);
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < KT / 8; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float pv = exp2f(s[j][2 * h + e] - msafe);
+        s[j][2 * h + e] = pv;
+        sum += pv;
+      }
+    }
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    lrow[h] = lrow[h] * corr + sum;
+    mrow[h] = mnew;
+#pragma unroll
+    for (int n = 0; n < HD / 8; ++n) {
+      o[n][2 * h] *= corr;
+      o[n][2 * h + 1] *= corr;
+    }
+  }
+}
+
+// load the warp's 16 packed Q rows from a swizzled smem tile into fragments
+template <int HD>
+__device__ __forceinline__ void load_q_frags(uint32_t (&qf)[HD / 16][4], const __nv_bfloat16* sQ,
+                                             int row0, int lane) {
+#pragma unroll
+  for (int ks = 0; ks < HD / 16; ++ks) {
+    ldmatrix_x4(tile_addr<HD>(sQ, row0 + (lane & 15), ks * 2 + (lane >> 4)), qf[ks][0], qf[ks][1],
+                qf[ks][2], qf[ks][3]);
+  }
+}
+
+// ================================================================ prefill
+constexpr int PF_WARPS = 4;
+constexpr int PF_ROWS = 16 * PF_WARPS;  // packed rows per CTA
+constexpr int PF_KT = 64;
+
+template <int HD>
+__global__ void __launch_bounds__(PF_WARPS * 32) prefill_kernel(Params p) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+  __nv_bfloat16* sK = sQ + PF_ROWS * HD;        // [2][KT][HD]
+  __nv_bfloat16* sV = sK + 2 * PF_KT * HD;      // [2][KT][HD]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int2 wk = p.work[blockIdx.x];
+  const int item = wk.x, tok0 = wk.y;
+  const int kvh = blockIdx.y;
+  const int G = p.group;
+  const int q_row0 = p.cu_q[item];
+  const int q_len = p.cu_q[item + 1] - q_row0;
+  const int fpos = p.first_pos[item];
+  const int kv_len = p.kv_len[item];
+  const int32_t* bt = p.block_tables + (int64_t)item * p.bt_stride;
+  const int tok_per_cta = PF_ROWS / G;
+  const int tok_last = min(tok0 + tok_per_cta, q_len) - 1;
+  const int kv_end = min(kv_len, fpos + tok_last + 1);
+  const int n_kt = (kv_end + PF_KT - 1) / PF_KT;
+
+  // ---- Q tile (packed rows r -> token tok0 + r / G, head kvh*G + r % G)
+  constexpr int NCH = HD / 8;
+  for (int i = tid; i < PF_ROWS * NCH; i += PF_WARPS * 32) {
+    const int r = i / NCH, c = i % NCH;
+    const int t = tok0 + r / G;
+    const bool ok = t < q_len;
+    const __nv_bfloat16* src = p.q;
+    if (ok) src = p.q + (int64_t)(q_row0 + t) * p.ldq + (int64_t)(kvh * G + r % G) * HD + c * 8;
+    cp_async16(sQ + r * HD + swz<HD>(r, c) * 8, src, ok);
+  }
+  load_kv_tile<HD>(sK, p.k_pool, bt, kvh, p.kv_heads, p.block_size, 0, PF_KT, kv_end, tid,
+                   PF_WARPS * 32);
+  load_kv_tile<HD>(sV, p.v_pool, bt, kvh, p.kv_heads, p.block_size, 0, PF_KT, kv_end, tid,
+                   PF_WARPS * 32);
+  cp_async_commit();
+
+  const int rowA = warp * 16 + (lane >> 2);  // packed rows held by this thread
+  int limit[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int t = tok0 + (rowA + 8 * h) / G;
+    limit[h] = fpos + min(t, q_len - 1);
+  }
+  const int min_limit = fpos + tok0;
+
+  float o[HD / 8][4];
+#pragma unroll
+  for (int n = 0; n < HD / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+  uint32_t qf[HD / 16][4];
+
+  for (int kt = 0; kt < n_kt; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < n_kt) {
+      load_kv_tile<HD>(sK + (buf ^ 1) * PF_KT * HD, p.k_pool, bt, kvh, p.kv_heads, p.block_size,
+                       (kt + 1) * PF_KT, PF_KT, kv_end, tid, PF_WARPS * 32);
+      load_kv_tile<HD>(sV + (buf ^ 1) * PF_KT * HD, p.v_pool, bt, kvh, p.kv_heads, p.block_size,
+                       (kt + 1) * PF_KT, PF_KT, kv_end, tid, PF_WARPS * 32);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (kt == 0) load_q_frags<HD>(qf, sQ, warp * 16, lane);
+    float s[PF_KT / 8][4];
+    qk_tile<HD, PF_KT>(s, qf, sK + buf * PF_KT * HD, lane);
+    const int kbase = kt * PF_KT;
+    const bool need_mask = kbase + PF_KT - 1 > min_limit;
+    softmax_update<HD, PF_KT>(s, o, mrow, lrow, kbase, limit, need_mask, p.scale_log2, lane);
+    pv_tile<HD, PF_KT>(o, s, sV + buf * PF_KT * HD, lane);
+    __syncthreads();
+  }
+
+  // ---- normalise and store
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = rowA + 8 * h;
+    const int t = tok0 + r / G;
+    if (t >= q_len) continue;
+    const float inv = 1.f / lrow[h];
+    __nv_bfloat16* dst = p.out + (int64_t)(q_row0 + t) * p.ldo + (int64_t)(kvh * G + r % G) * HD;
+#pragma unroll
+    for (int n = 0; n < HD / 8; ++n) {
+      *reinterpret_cast<uint32_t*>(dst + n * 8 + (lane & 3) * 2) =
+          pack_bf16x2(o[n][2 * h] * inv, o[n][2 * h + 1] * inv);
+    }
+  }
+}
+
+// ================================================================= decode
+constexpr int DC_WARPS = 4;
+constexpr int DC_KT = 32;
+
+template <int HD>
+__global__ void __launch_bounds__(DC_WARPS * 32) decode_kernel(Params p) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(smem_raw) + warp * (4 * DC_KT * HD);
+  __nv_bfloat16* sV = sK + 2 * DC_KT * HD;
+  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw) + DC_WARPS * 4 * DC_KT * HD;
+
+  const int item = blockIdx.x, kvh = blockIdx.y, split = blockIdx.z;
+  const int G = p.group;
+  const int q_row = p.cu_q[item];
+  const int kv_len = p.kv_len[item];
+  const int32_t* bt = p.block_tables + (int64_t)item * p.bt_stride;
+  const int n_tiles = (kv_len + DC_KT - 1) / DC_KT;
+  const int per_split = (n_tiles + p.n_splits - 1) / p.n_splits;
+  const int t_begin = split * per_split;
+  const int t_end = min(n_tiles, t_begin + per_split);
+
+  // ---- packed Q rows (G heads of the single query token), rows >= G are zero
+  constexpr int NCH = HD / 8;
+  for (int i = tid; i < 16 * NCH; i += DC_WARPS * 32) {
+    const int r = i / NCH, c = i % NCH;
+    const bool ok = r < G;
+    const __nv_bfloat16* src = p.q;
+    if (ok) src = p.q + (int64_t)q_row * p.ldq + (int64_t)(kvh * G + r) * HD + c * 8;
+    cp_async16(sQ + r * HD + swz<HD>(r, c) * 8, src, ok);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  uint32_t qf[HD / 16][4];
+  load_q_frags<HD>(qf, sQ, 0, lane);
+
+  float o[HD / 8][4];
+#pragma unroll
+  for (int n = 0; n < HD / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+  const int limit[2] = {kv_len - 1, kv_len - 1};
+
+  int kt = t_begin + warp;
+  if (kt < t_end) {
+    load_kv_tile<HD>(sK, p.k_pool, bt, kvh, p.kv_heads, p.block_size, kt * DC_KT, DC_KT, kv_len,
+                     lane, 32);
+    load_kv_tile<HD>(sV, p.v_pool, bt, kvh, p.kv_heads, p.block_size, kt * DC_KT, DC_KT, kv_len,
+                     lane, 32);
+  }
+  cp_async_commit();
+  int buf = 0;
+  for (; kt < t_end; kt += DC_WARPS) {
+    const int nxt = kt + DC_WARPS;
+    if (nxt < t_end) {
+      load_kv_tile<HD>(sK + (buf ^ 1) * DC_KT * HD, p.k_pool, bt, kvh, p.kv_heads, p.block_size,
+                       nxt * DC_KT, DC_KT, kv_len, lane, 32);
+      load_kv_tile<HD>(sV + (buf ^ 1) * DC_KT * HD, p.v_pool, bt, kvh, p.kv_heads, p.block_size,
+                       nxt * DC_KT, DC_KT, kv_len, lane, 32);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    float s[DC_KT / 8][4];
+    qk_tile<HD, DC_KT>(s, qf, sK + buf * DC_KT * HD, lane);
+    const int kbase = kt * DC_KT;
+    softmax_update<HD, DC_KT>(s, o, mrow, lrow, kbase, limit, kbase + DC_KT > kv_len, p.scale_log2,
+                              lane);
+    pv_tile<HD, DC_KT>(o, s, sV + buf * DC_KT * HD, lane);
+    __syncwarp();
+    buf ^= 1;
+  }
+  cp_async_wait<0>();
+  __syncthreads();  // all warps done with their smem tiles -> reuse as merge scratch
+
+  // ---- merge warps: rows 0..G-1 live in thread rows lane>>2 (h=0)
+  float* sm = reinterpret_cast<float*>(smem_raw);  // [warps][16] m, [warps][16] l, [warps][16][HD] o
+  float* sl = sm + DC_WARPS * 16;
+  float* so = sl + DC_WARPS * 16;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = (lane >> 2) + 8 * h;
+    if ((lane & 3) == 0) {
+      sm[warp * 16 + r] = mrow[h];
+      sl[warp * 16 + r] = lrow[h];
+    }
+#pragma unroll
+    for (int n = 0; n < HD / 8; ++n) {
+      so[(warp * 16 + r) * HD + n * 8 + (lane & 3) * 2] = o[n][2 * h];
+      so[(warp * 16 + r) * HD + n * 8 + (lane & 3) * 2 + 1] = o[n][2 * h + 1];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < G * HD; i += DC_WARPS * 32) {
+    const int row = i / HD, c = i % HD;
+    float mx = -INFINITY;
+    for (int w = 0; w < DC_WARPS; ++w) mx = fmaxf(mx, sm[w * 16 + row]);
+    float l = 0.f, acc = 0.f;
+    if (mx != -INFINITY) {
+      for (int w = 0; w < DC_WARPS; ++w) {
+        const float f = exp2f(sm[w * 16 + row] - mx);
+        l += sl[w * 16 + row] * f;
+        acc += so[(w * 16 + row) * HD + c] * f;
+      }
+    }
+    const int qh = kvh * G + row;
+    if (p.n_splits == 1) {
+      p.out[(int64_t)q_row * p.ldo + (int64_t)qh * HD + c] = __float2bfloat16_rn(acc / l);
+    } else {
+      const int64_t slot = ((int64_t)item * p.q_heads + qh) * p.n_splits + split;
+      p.ws_o[slot * HD + c] = l > 0.f ? acc / l : 0.f;
+      if (c == 0) p.ws_lse[slot] = l > 0.f ? mx + log2f(l) : -INFINITY;
+    }
+  }
+}
+
+__global__ void combine_kernel(Params p, int head_dim) {
+  const int item = blockIdx.x, qh = blockIdx.y;
+  const int64_t base = ((int64_t)item * p.q_heads + qh) * p.n_splits;
+  float mx = -INFINITY;
+  for (int s = 0; s < p.n_splits; ++s) mx = fmaxf(mx, p.ws_lse[base + s]);
+  const int q_row = p.cu_q[item];
+  for (int c = threadIdx.x; c < head_dim; c += blockDim.x) {
+    float w = 0.f, acc = 0.f;
+    for (int s = 0; s < p.n_splits; ++s) {
+      const float l = p.ws_lse[base + s];
+      if (l == -INFINITY) continue;
+      const float f = exp2f(l - mx);
+      w += f;
+      acc += f * p.ws_o[(base + s) * head_dim + c];
+    }
+    p.out[(int64_t)q_row * p.ldo + (int64_t)qh * head_dim + c] = __float2bfloat16_rn(acc / w);
+  }
+}
+
+template <int HD>
+static int launch(const Params& p, int n_items, int n_work, cudaStream_t st) {
+  if (n_work > 0) {
+    const int smem = (PF_ROWS * HD + 4 * PF_KT * HD) * 2;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(prefill_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+    prefill_kernel<HD><<<dim3(n_work, p.kv_heads), PF_WARPS * 32, smem, st>>>(p);
+    return check_launch("attn_prefill_kernel");
+  }
+  const int smem_tiles = (DC_WARPS * 4 * DC_KT * HD + 16 * HD) * 2;
+  const int smem_merge = (DC_WARPS * 32 + DC_WARPS * 16 * HD) * 4;
+  const int smem = smem_tiles > smem_merge ? smem_tiles : smem_merge;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(decode_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  decode_kernel<HD><<<dim3(n_items, p.kv_heads, p.n_splits), DC_WARPS * 32, smem, st>>>(p);
+  if (int rc = check_launch("attn_decode_kernel")) return rc;
+  if (p.n_splits > 1) {
+    combine_kernel<<<dim3(n_items, p.q_heads), HD, 0, st>>>(p, HD);
+    return check_launch("attn_combine_kernel");
+  }
+  return kOk;
+}
+
+static int decode_splits(int n_items, int kv_heads, int max_kv_len) {
+  const int ctas = n_items * kv_heads;
+  int want = (2 * 148 + ctas - 1) / ctas;
+  const int max_useful = (max_kv_len + DC_WARPS * DC_KT - 1) / (DC_WARPS * DC_KT);
+  if (want > max_useful) want = max_useful;
+  if (want > 64) want = 64;
+  return want < 1 ? 1 : want;
+}
+
+}  // namespace attn
+}  // namespace sp
+
+using namespace sp;
+
+extern "C" int sp_attn_tile_tokens(int q_heads, int kv_heads) {
+  if (kv_heads <= 0 || q_heads % kv_heads) return 0;
+  const int g = q_heads / kv_heads;
+  return g > attn::PF_ROWS ? 0 : attn::PF_ROWS / g;
+}
+
+extern "C" int64_t sp_attn_workspace_bytes(int n_items, int q_heads, int head_dim, int max_kv_len) {
+  (void)max_kv_len;
+  const int64_t splits = 64;
+  return (int64_t)n_items * q_heads * splits * (head_dim + 1) * 4;
+}
+
+extern "C" sp_status sp_attention(const void* q, int64_t ldq, const void* k_pool, const void* v_pool,
+                                  const int32_t* block_tables, int64_t bt_stride, const int32_t* cu_q,
+                                  const int32_t* first_pos, const int32_t* kv_len, int n_items,
+                                  const int32_t* work, int n_work, int max_q_len, int max_kv_len,
+                                  void* out, int64_t ldo, int q_heads, int kv_heads, int head_dim,
+                                  int block_size, void* ws, int64_t ws_bytes, void* stream) {
+  (void)max_q_len;
+  if (n_items < 0 || n_work < 0) return fail(kInvalid, "attention: negative sizes");
+  if (n_items == 0) return kOk;
+  if (kv_heads <= 0 || q_heads % kv_heads) return fail(kInvalid, "attention: q_heads % kv_heads != 0");
+  const int G = q_heads / kv_heads;
+  if (G > 16) return fail(kUnsupported, "attention: GQA group > 16");
+  if (ldq % 8 || ldo % 2) return fail(kInvalid, "attention: bad row strides");
+  if (block_size <= 0) return fail(kInvalid, "attention: bad block size");
+  attn::Params p;
+  p.q = static_cast<const __nv_bfloat16*>(q);
+  p.ldq = ldq;
+  p.k_pool = static_cast<const __nv_bfloat16*>(k_pool);
+  p.v_pool = static_cast<const __nv_bfloat16*>(v_pool);
+  p.block_tables = block_tables;
+  p.bt_stride = bt_stride;
+  p.cu_q = cu_q;
+  p.first_pos = first_pos;
+  p.kv_len = kv_len;
+  p.work = reinterpret_cast<const int2*>(work);
+  p.out = static_cast<__nv_bfloat16*>(out);
+  p.ldo = ldo;
+  p.q_heads = q_heads;
+  p.kv_heads = kv_heads;
+  p.group = G;
+  p.block_size = block_size;
+  p.scale_log2 = attn::kLog2e / sqrtf((float)head_dim);
+  p.n_splits = 1;
+  p.ws_o = nullptr;
+  p.ws_lse = nullptr;
+  if (n_work == 0) {
+    p.n_splits = attn::decode_splits(n_items, kv_heads, max_kv_len);
+    if (p.n_splits > 1) {
+      const int64_t need = (int64_t)n_items * q_heads * p.n_splits * (head_dim + 1) * 4;
+      if (!ws || ws_bytes < need) {
+        p.n_splits = 1;
+      } else {
+        p.ws_o = static_cast<float*>(ws);
+        p.ws_lse = p.ws_o + (int64_t)n_items * q_heads * p.n_splits * head_dim;
+      }
+    }
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  switch (head_dim) {
+    case 32: return attn::launch<32>(p, n_items, n_work, st);
+    case 64: return attn::launch<64>(p, n_items, n_work, st);
+    case 128: return attn::launch<128>(p, n_items, n_work, st);
+    default: return fail(kUnsupported, "attention: head_dim must be 32, 64 or 128");
+  }
+}

@@ -1,0 +1,386 @@
+// Error plumbing, device check and the small HBM-bound kernels of the path:
+// embedding gather, fused residual-add + RMSNorm, RoPE + paged KV write,
+// all-to-all pack/unpack, loopback add, argmax and row gather.
+#include <cstdio>
+#include <string>
+
+#include "../../include/shiftpar.h"
+#include "common.cuh"
+
+namespace sp {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(kCuda, std::string(what) + ": " + cudaGetErrorString(e));
+  return kOk;
+}
+
+// ----------------------------------------------------------------- embedding
+__global__ void embed_kernel(const int32_t* __restrict__ ids, const __nv_bfloat16* __restrict__ table,
+                             const int32_t* __restrict__ pos, const float* __restrict__ pos_table,
+                             float* __restrict__ out, int hidden) {
+  const int r = blockIdx.x;
+  const int64_t tok = ids[r];
+  const __nv_bfloat16* src = table + tok * hidden;
+  float* dst = out + (int64_t)r * hidden;
+  const float* pt = pos_table ? pos_table + (int64_t)pos[r] * hidden : nullptr;
+  for (int c = threadIdx.x * 8; c < hidden; c += blockDim.x * 8) {
+    uint4 u = *reinterpret_cast<const uint4*>(src + c);
+    float2 a = unpack_bf16x2(u.x), b = unpack_bf16x2(u.y), e = unpack_bf16x2(u.z),
+           f = unpack_bf16x2(u.w);
+    float v[8] = {a.x, a.y, b.x, b.y, e.x, e.y, f.x, f.y};
+    if (pt) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] += pt[c + j];
+    }
+    reinterpret_cast<float4*>(dst + c)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(dst + c)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+
+// ------------------------------------------------------- add + rmsnorm
+template <int VEC>
+__global__ void add_rmsnorm_kernel(float* __restrict__ x, int64_t ldx, const float* __restrict__ add,
+                                   const float* __restrict__ gain, float eps,
+                                   const int32_t* __restrict__ row_idx,
+                                   __nv_bfloat16* __restrict__ out, int64_t ldo, int hidden) {
+  const int r = blockIdx.x;
+  const int64_t src_row = row_idx ? row_idx[r] : r;
+  float* xr = x + src_row * ldx;
+  const float* ar = add ? add + (int64_t)r * hidden : nullptr;
+  float v[VEC * 4];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = (i * blockDim.x + threadIdx.x) * 4;
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c < hidden) {
+      t = *reinterpret_cast<const float4*>(xr + c);
+      if (ar) {
+        float4 a = *reinterpret_cast<const float4*>(ar + c);
+        t.x += a.x;
+        t.y += a.y;
+        t.z += a.z;
+        t.w += a.w;
+        *reinterpret_cast<float4*>(xr + c) = t;
+      }
+    }
+    v[4 * i + 0] = t.x;
+    v[4 * i + 1] = t.y;
+    v[4 * i + 2] = t.z;
+    v[4 * i + 3] = t.w;
+    ss += t.x * t.x + t.y * t.y + t.z * t.z + t.w * t.w;
+  }
+  __shared__ float red[32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) red[0] = s;
+  }
+  __syncthreads();
+  const float den = sqrtf(red[0] / (float)hidden + eps);
+  __nv_bfloat16* orow = out + (int64_t)r * ldo;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = (i * blockDim.x + threadIdx.x) * 4;
+    if (c < hidden) {
+      float4 g = *reinterpret_cast<const float4*>(gain + c);
+      uint2 u;
+      u.x = pack_bf16x2(g.x * (v[4 * i + 0] / den), g.y * (v[4 * i + 1] / den));
+      u.y = pack_bf16x2(g.z * (v[4 * i + 2] / den), g.w * (v[4 * i + 3] / den));
+      *reinterpret_cast<uint2*>(orow + c) = u;
+    }
+  }
+}
+
+// ------------------------------------------------- RoPE + paged KV write
+// one warp per (token, head); lanes cover the d/2 rotation pairs
+__global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldqkv,
+                               const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,
+                               const float* __restrict__ rope, __nv_bfloat16* __restrict__ q_out,
+                               int64_t ldq, __nv_bfloat16* __restrict__ k_pool,
+                               __nv_bfloat16* __restrict__ v_pool, int rows, int q_heads,
+                               int kv_heads, int head_dim, int block_size) {
+  const int heads = q_heads + 2 * kv_heads;
+  const int warps_per_block = blockDim.x >> 5;
+  const int64_t item = (int64_t)blockIdx.x * warps_per_block + (threadIdx.x >> 5);
+  if (item >= (int64_t)rows * heads) return;
+  const int r = (int)(item / heads);
+  const int h = (int)(item % heads);
+  const int lane = threadIdx.x & 31;
+  const int half = head_dim >> 1;
+  const __nv_bfloat16* src = qkv + (int64_t)r * ldqkv + (int64_t)h * head_dim;
+  __nv_bfloat16* dst;
+  if (h < q_heads) {
+    if (!q_out) return;
+    dst = q_out + (int64_t)r * ldq + (int64_t)h * head_dim;
+  } else {
+    const int s = slot[r];
+    if (s < 0) return;
+    const int kvh = (h - q_heads) % kv_heads;
+    __nv_bfloat16* pool = (h - q_heads) < kv_heads ? k_pool : v_pool;
+    const int64_t blk = s / block_size, off = s % block_size;
+    dst = pool + ((blk * kv_heads + kvh) * block_size + off) * head_dim;
+  }
+  const bool rotate = rope != nullptr && h < q_heads + kv_heads;
+  const float* cs = rotate ? rope + (int64_t)pos[r] * half * 2 : nullptr;
+  for (int i = lane; i < half; i += 32) {
+    float a = __bfloat162float(src[i]);
+    float b = __bfloat162float(src[i + half]);
+    if (rotate) {
+      const float c = cs[2 * i], s = cs[2 * i + 1];
+      const float na = a * c - b * s;
+      const float nb = b * c + a * s;
+      a = na;
+      b = nb;
+    }
+    dst[i] = __float2bfloat16_rn(a);
+    dst[i + half] = __float2bfloat16_rn(b);
+  }
+}
+
+// ------------------------------------------------------ a2a pack/unpack
+__global__ void pack_kernel(const uint4* __restrict__ src, int64_t lds_v, uint4* __restrict__ dst,
+                            int rows, int peers, int width_v) {
+  const int64_t total = (int64_t)rows * peers * width_v;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i % width_v;
+    const int64_t r = (i / width_v) % rows;
+    const int64_t p = i / ((int64_t)width_v * rows);
+    dst[i] = src[r * lds_v + p * width_v + c];
+  }
+}
+
+__global__ void unpack_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int64_t ldd_v,
+                              int rows, int peers, int width_v) {
+  const int64_t total = (int64_t)rows * peers * width_v;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i % width_v;
+    const int64_t p = (i / width_v) % peers;
+    const int64_t r = i / ((int64_t)width_v * peers);
+    dst[r * ldd_v + p * width_v + c] = src[(p * rows + r) * width_v + c];
+  }
+}
+
+// ------------------------------------------------------------ small ops
+__global__ void add_f32_kernel(const float4* __restrict__ a, const float4* __restrict__ b,
+                               float4* __restrict__ d, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 x = a[i], y = b[i];
+    d[i] = make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
+  }
+}
+
+__global__ void add_f32_tail_kernel(const float* a, const float* b, float* d, int64_t lo, int64_t n) {
+  int64_t i = lo + threadIdx.x;
+  if (i < n) d[i] = a[i] + b[i];
+}
+
+__global__ void argmax_kernel(const float* __restrict__ logits, int64_t ld, int vocab,
+                              int32_t* __restrict__ idx, float* __restrict__ val) {
+  const float* row = logits + (int64_t)blockIdx.x * ld;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
+    float x = row[i];
+    if (x > best || (x == best && i < bi)) {
+      best = x;
+      bi = i;
+    }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = best;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x >> 5;
+    best = threadIdx.x < nw ? sv[threadIdx.x] : -INFINITY;
+    bi = threadIdx.x < nw ? si[threadIdx.x] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) {
+        best = ov;
+        bi = oi;
+      }
+    }
+    if (threadIdx.x == 0) {
+      idx[blockIdx.x] = bi;
+      if (val) val[blockIdx.x] = best;
+    }
+  }
+}
+
+__global__ void gather_rows_kernel(const float* __restrict__ src, int64_t lds,
+                                   const int32_t* __restrict__ idx, float* __restrict__ dst,
+                                   int64_t ldd, int width) {
+  const float* s = src + (int64_t)idx[blockIdx.x] * lds;
+  float* d = dst + (int64_t)blockIdx.x * ldd;
+  for (int c = threadIdx.x; c < width; c += blockDim.x) d[c] = s[c];
+}
+
+static int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > 148 * 16) g = 148 * 16;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace sp
+
+using namespace sp;
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" const char* sp_last_error(void) { return sp::g_err.c_str(); }
+
+extern "C" int sp_abi_version(void) { return 1; }
+
+extern "C" sp_status sp_device_check(int* sm_count) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(kCuda, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  int major = 0, minor = 0, sms = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sm_count) *sm_count = sms;
+  if (major != 10 || minor != 0)
+    return fail(kUnsupported, "libshiftpar is built for sm_100a (B200); device is sm_" +
+                                  std::to_string(major) + std::to_string(minor));
+  return kOk;
+}
+
+extern "C" sp_status sp_embed(const int32_t* ids, const void* table_bf16, const int32_t* pos,
+                              const float* pos_table, float* out_f32, int rows, int hidden,
+                              void* stream) {
+  if (rows < 0 || hidden <= 0 || hidden % 8) return fail(kInvalid, "embed: hidden % 8 != 0");
+  if (rows == 0) return kOk;
+  if (pos_table && !pos) return fail(kInvalid, "embed: pos_table without positions");
+  embed_kernel<<<rows, 128, 0, S(stream)>>>(ids, static_cast<const __nv_bfloat16*>(table_bf16), pos,
+                                            pos_table, out_f32, hidden);
+  return check_launch("embed_kernel");
+}
+
+extern "C" sp_status sp_add_rmsnorm(float* x, int64_t ldx, const float* add, const float* gain,
+                                    float eps, const int32_t* row_idx, void* out_bf16, int64_t ldo,
+                                    int rows, int hidden, void* stream) {
+  if (rows < 0 || hidden <= 0 || hidden % 4 || ldx % 4 || ldo % 4)
+    return fail(kInvalid, "add_rmsnorm: hidden and strides must be multiples of 4");
+  if (rows == 0) return kOk;
+  if (add && row_idx) return fail(kInvalid, "add_rmsnorm: add with row_idx unsupported");
+  const int threads = 256;
+  const int per = (hidden + threads * 4 - 1) / (threads * 4);
+  auto out = static_cast<__nv_bfloat16*>(out_bf16);
+  switch (per) {
+    case 1: add_rmsnorm_kernel<1><<<rows, threads, 0, S(stream)>>>(x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
+    case 2: add_rmsnorm_kernel<2><<<rows, threads, 0, S(stream)>>>(x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
+    case 3: add_rmsnorm_kernel<3><<<rows, threads, 0, S(stream)>>>(x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
+    case 4: add_rmsnorm_kernel<4><<<rows, threads, 0, S(stream)>>>(x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
+    case 5: case 6: case 7: case 8:
+      add_rmsnorm_kernel<8><<<rows, threads, 0, S(stream)>>>(x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
+    default: return fail(kUnsupported, "add_rmsnorm: hidden > 8192");
+  }
+  return check_launch("add_rmsnorm_kernel");
+}
+
+extern "C" sp_status sp_rope_kv_write(const void* qkv, int64_t ldqkv, const int32_t* pos,
+                                      const int32_t* slot, const float* rope_table, void* q_out,
+                                      int64_t ldq, void* k_pool, void* v_pool, int rows,
+                                      int q_heads, int kv_heads, int head_dim, int block_size,
+                                      void* stream) {
+  if (rows < 0 || q_heads < 0 || kv_heads < 0 || head_dim <= 0 || head_dim % 2 || block_size <= 0)
+    return fail(kInvalid, "rope_kv_write: bad geometry");
+  if (rows == 0 || q_heads + kv_heads == 0) return kOk;
+  if (kv_heads > 0 && (!k_pool || !v_pool || !slot)) return fail(kInvalid, "rope_kv_write: null pool/slot");
+  const int heads = q_heads + 2 * kv_heads;
+  const int64_t warps = (int64_t)rows * heads;
+  const int wpb = 8;
+  rope_kv_kernel<<<(unsigned)((warps + wpb - 1) / wpb), wpb * 32, 0, S(stream)>>>(
+      static_cast<const __nv_bfloat16*>(qkv), ldqkv, pos, slot, rope_table,
+      static_cast<__nv_bfloat16*>(q_out), ldq, static_cast<__nv_bfloat16*>(k_pool),
+      static_cast<__nv_bfloat16*>(v_pool), rows, q_heads, kv_heads, head_dim, block_size);
+  return check_launch("rope_kv_kernel");
+}
+
+extern "C" sp_status sp_a2a_pack(const void* src, int64_t lds, void* dst, int rows, int peers,
+                                 int width, void* stream) {
+  if (rows < 0 || peers <= 0 || width <= 0 || width % 8 || lds % 8)
+    return fail(kInvalid, "a2a_pack: width and stride must be multiples of 8");
+  if (rows == 0) return kOk;
+  const int64_t n = (int64_t)rows * peers * (width / 8);
+  pack_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(static_cast<const uint4*>(src), lds / 8,
+                                                      static_cast<uint4*>(dst), rows, peers, width / 8);
+  return check_launch("pack_kernel");
+}
+
+extern "C" sp_status sp_a2a_unpack(const void* src, void* dst, int64_t ldd, int rows, int peers,
+                                   int width, void* stream) {
+  if (rows < 0 || peers <= 0 || width <= 0 || width % 8 || ldd % 8)
+    return fail(kInvalid, "a2a_unpack: width and stride must be multiples of 8");
+  if (rows == 0) return kOk;
+  const int64_t n = (int64_t)rows * peers * (width / 8);
+  unpack_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(static_cast<const uint4*>(src),
+                                                        static_cast<uint4*>(dst), ldd / 8, rows,
+                                                        peers, width / 8);
+  return check_launch("unpack_kernel");
+}
+
+extern "C" sp_status sp_add_f32(const float* a, const float* b, float* dst, int64_t n, void* stream) {
+  if (n < 0) return fail(kInvalid, "add_f32: n < 0");
+  if (n == 0) return kOk;
+  if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
+       reinterpret_cast<uintptr_t>(dst)) & 15)
+    return fail(kInvalid, "add_f32: pointers must be 16-byte aligned");
+  const int64_t n4 = n / 4;
+  if (n4) add_f32_kernel<<<grid_for(n4, 256), 256, 0, S(stream)>>>(
+      reinterpret_cast<const float4*>(a), reinterpret_cast<const float4*>(b),
+      reinterpret_cast<float4*>(dst), n4);
+  if (n % 4) add_f32_tail_kernel<<<1, 32, 0, S(stream)>>>(a, b, dst, n4 * 4, n);
+  return check_launch("add_f32_kernel");
+}
+
+extern "C" sp_status sp_argmax(const float* logits, int64_t ld, int rows, int vocab, int32_t* idx,
+                               float* val, void* stream) {
+  if (rows < 0 || vocab <= 0) return fail(kInvalid, "argmax: bad shape");
+  if (rows == 0) return kOk;
+  argmax_kernel<<<rows, 1024, 0, S(stream)>>>(logits, ld, vocab, idx, val);
+  return check_launch("argmax_kernel");
+}
+
+extern "C" sp_status sp_gather_rows_f32(const float* src, int64_t lds, const int32_t* idx, float* dst,
+                                        int64_t ldd, int rows, int width, void* stream) {
+  if (rows < 0 || width <= 0) return fail(kInvalid, "gather_rows: bad shape");
+  if (rows == 0) return kOk;
+  gather_rows_kernel<<<rows, 256, 0, S(stream)>>>(src, lds, idx, dst, ldd, width);
+  return check_launch("gather_rows_kernel");
+}

@@ -1,0 +1,863 @@
+"""Shift-Parallel engine on B200: per-pass SP/TP over one head-sharded paged KV pool.
+
+Drop-in for the reference engine API (/root/reference/pkg/src/shiftsim/
+parallel_engine.py): ``Engine(weights, group, policy, swiftkv)`` (:194-216),
+``new_sequence`` (:220-227), ``step(batch, mode=None, span_logits=False) ->
+(logits per item, StepRecord)`` (:231-282), ``choose_mode`` (:134-145) and
+the ``Batch`` / ``BatchItem`` / ``Sequence`` / ``ShiftPolicy`` types (:63-127).
+
+What runs where (all arithmetic is libshiftpar.so, sm_100a):
+
+TP pass (:333-398)  x replicated [M, h] f32; per rank r: QKV GEMM on the rank's
+    rows of the fused weight -> RoPE + paged KV write -> attention over owned
+    heads -> O GEMM on the rank's K window -> NCCL all-reduce -> fused
+    add+RMSNorm -> SwiGLU GEMM on owned ffn rows -> down GEMM -> all-reduce.
+    The embedding uses the resident replica (no all-reduce, containment
+    model.py:257-281); at P = 1 the partials add straight into x in the GEMM
+    epilogue.
+SP pass (:454-537)  tokens of the flattened batch split contiguously; per rank:
+    RMSNorm -> full-replica QKV GEMM whose epilogue writes each peer's head
+    block into a contiguous send buffer -> ONE all-to-all (q|k|v fused) ->
+    the same RoPE/KV-write and attention kernels as TP (the received layout is
+    identical to a TP rank's QKV output) -> all-to-all back -> O GEMM reading
+    the per-peer receive layout through a 3-D TMA map, adding into x ->
+    RMSNorm -> SwiGLU -> down GEMM adding into x.
+Both modes write identical K/V rows to the same per-device blocks, so the
+mode can change every pass with zero KV movement (kv_cache.py:1-15).
+"""
+
+from __future__ import annotations
+
+import enum
+import time
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence as Seq, Tuple
+
+import numpy as np
+import torch
+
+from . import ops
+from .config import ModelConfig
+from .errors import CacheOverflow, ConfigError, ContractViolation
+from .fabric import CommRecord, DeviceGroup, LoopbackGroup
+from .flops import FlopMeter, PassShape, shard_bounds, shard_rows
+from .kv_cache import KvCache, KvPool
+from .weights import ModelWeights
+
+
+class ParallelMode(enum.Enum):
+    TP = "tp"
+    SP = "sp"
+
+
+class BatchKind(enum.Enum):
+    PREFILL = "prefill"
+    DECODE = "decode"
+
+
+@dataclass
+class Sequence:
+    """Engine-side identity of one request: an id plus its KV cache (:63-68)."""
+
+    seq_id: int
+    cache: KvCache
+
+
+@dataclass
+class BatchItem:
+    seq: Sequence
+    tokens: List[int]
+
+
+@dataclass
+class Batch:
+    kind: BatchKind
+    items: List[BatchItem]
+    speculative: bool = False
+
+    @property
+    def total_new_tokens(self) -> int:
+        return sum(len(it.tokens) for it in self.items)
+
+    def validate(self) -> None:
+        """parallel_engine.py:88-99."""
+        if not self.items:
+            raise ContractViolation("batch must contain at least one item")
+        for it in self.items:
+            if len(it.tokens) < 1:
+                raise ContractViolation("batch item with empty span")
+        if self.kind is BatchKind.DECODE and not self.speculative:
+            if any(len(it.tokens) != 1 for it in self.items):
+                raise ContractViolation("decode batches carry exactly 1 new token per request")
+        if len({id(it.seq.cache) for it in self.items}) != len(self.items):
+            raise ContractViolation("a sequence may appear at most once per batch")
+
+
+@dataclass(frozen=True)
+class ShiftPolicy:
+    """SP at or above ``token_threshold`` new tokens, TP below (:102-127)."""
+
+    token_threshold: Optional[int] = None
+    kind: str = "shift"
+
+    def validate(self) -> "ShiftPolicy":
+        if self.kind not in ("fixed_tp", "fixed_sp", "shift"):
+            raise ConfigError(f"unknown policy kind {self.kind!r}")
+        if self.kind == "shift" and (self.token_threshold is None or self.token_threshold < 1):
+            raise ConfigError("shift policy needs token_threshold >= 1")
+        return self
+
+    @staticmethod
+    def fixed_tp() -> "ShiftPolicy":
+        return ShiftPolicy(kind="fixed_tp")
+
+    @staticmethod
+    def fixed_sp() -> "ShiftPolicy":
+        return ShiftPolicy(kind="fixed_sp")
+
+
+def default_token_threshold(world_size: int) -> int:
+    """The reference default 4·P (:130-131); see DESIGN.md for the B200 crossover."""
+    return 4 * world_size
+
+
+def choose_mode(policy: ShiftPolicy, batch: Batch) -> ParallelMode:
+    policy.validate()
+    if policy.kind == "fixed_tp":
+        return ParallelMode.TP
+    if policy.kind == "fixed_sp":
+        return ParallelMode.SP
+    return ParallelMode.SP if batch.total_new_tokens >= policy.token_threshold else ParallelMode.TP
+
+
+@dataclass(frozen=True)
+class SwiftKvConfig:
+    """Early-exit prefill (reference swiftkv.py:26-46)."""
+
+    enabled: bool = False
+    cut_layer: Optional[int] = None
+
+    def resolve_cut(self, n_layers: int) -> int:
+        if not self.enabled:
+            return n_layers
+        cut = n_layers // 2 if self.cut_layer is None else self.cut_layer
+        if not 1 <= cut <= n_layers:
+            raise ConfigError(f"cut_layer {cut} outside [1, {n_layers}]")
+        return cut
+
+
+@dataclass(frozen=True)
+class CommEvent:
+    kind: str
+    bytes: float
+
+
+@dataclass(frozen=True)
+class StepRecord:
+    """parallel_engine.py:156-176 (+ host wall time of the enqueue)."""
+
+    step_id: int
+    mode: ParallelMode
+    kind: BatchKind
+    new_tokens: int
+    n_requests: int
+    flops_per_device: Tuple[int, ...]
+    comm: Tuple[CommEvent, ...]
+    host_ms: float = 0.0
+
+    @property
+    def flops_total(self) -> int:
+        return sum(self.flops_per_device)
+
+    @property
+    def flops_max_device(self) -> int:
+        return max(self.flops_per_device)
+
+    @property
+    def comm_bytes(self) -> float:
+        return sum(e.bytes for e in self.comm)
+
+
+def partition_heads(n_heads: int, world_size: int) -> Tuple[Tuple[int, int], ...]:
+    """Device d owns heads [d H/P, (d+1) H/P) (model.py:186-193)."""
+    if world_size < 1 or n_heads % world_size:
+        raise ConfigError(f"n_heads {n_heads} not divisible by world_size {world_size}")
+    w = n_heads // world_size
+    return tuple((r * w, (r + 1) * w) for r in range(world_size))
+
+
+class _Meta:
+    """Per-pass device metadata, uploaded with ONE host->device copy."""
+
+    pass
+
+
+class Engine:
+    def __init__(self, weights: ModelWeights, group: DeviceGroup, policy: ShiftPolicy,
+                 swiftkv: Optional[SwiftKvConfig] = None, *, num_blocks: Optional[int] = None,
+                 block_size: int = 64):
+        cfg = weights.config
+        self.weights = weights
+        self.config: ModelConfig = cfg
+        self.group = group
+        self.policy = policy.validate()
+        self.swiftkv = swiftkv if swiftkv is not None else SwiftKvConfig()
+        self.world_size = group.world_size
+        if weights.world_size != self.world_size:
+            raise ConfigError("weights were laid out for a different world size")
+        cfg.check_world(self.world_size)
+        self.partition = partition_heads(cfg.n_heads, self.world_size)
+        self.kv_partition = partition_heads(cfg.kv_heads, self.world_size)
+        self.device = weights.embed.device
+        ops.device_check()
+        if isinstance(group, LoopbackGroup):
+            group._add = ops.add_f32
+        if self.swiftkv.enabled:
+            cut = self.swiftkv.resolve_cut(cfg.n_layers)
+            if cut < cfg.n_layers:
+                weights.ensure_swiftkv(cut)
+        if num_blocks is None:
+            num_blocks = max(16, 4 * -(-cfg.max_seq // block_size))
+        self.pool = KvPool(cfg.n_layers, self.kv_partition, cfg.head_dim, num_blocks, block_size,
+                           group.local_ranks, self.device)
+        self.mode_log: List[ParallelMode] = []
+        self.step_records: List[StepRecord] = []
+        self._step_counter = 0
+        self._next_key = 0
+        self._pinned: List[torch.Tensor] = []
+        self._pin_events: List[Optional[torch.cuda.Event]] = []
+        self._pin_idx = 0
+        self._ws: Optional[torch.Tensor] = None
+
+    # ---------------------------------------------------------- sequences
+    def new_sequence(self, seq_id: int, capacity: Optional[int] = None) -> Sequence:
+        cap = self.config.max_seq if capacity is None else capacity
+        if cap > self.config.max_seq:
+            raise ContractViolation(f"capacity {cap} exceeds max_seq {self.config.max_seq}")
+        key = self._next_key
+        self._next_key += 1
+        return Sequence(seq_id=seq_id, cache=KvCache(self.pool, key, cap))
+
+    def release(self, seq: Sequence) -> None:
+        """Return a finished sequence's blocks to the pool (paged extension)."""
+        self.pool.alloc.release(seq.cache.key)
+        seq.cache.released = True
+
+    # --------------------------------------------------------------- step
+    def step(self, batch: Batch, mode: Optional[ParallelMode] = None,
+             span_logits: bool = False) -> Tuple[List[torch.Tensor], StepRecord]:
+        t_host = time.perf_counter()
+        batch.validate()
+        if mode is None:
+            mode = choose_mode(self.policy, batch)
+        for it in batch.items:
+            c = it.seq.cache
+            if c.released:
+                raise ContractViolation(f"sequence {it.seq.seq_id} was released")
+            if c.token_count + len(it.tokens) > c.capacity:
+                raise CacheOverflow(f"sequence {it.seq.seq_id}: {c.token_count + len(it.tokens)} "
+                                    f"tokens exceed capacity {c.capacity}")
+        cut_full = self.swiftkv.resolve_cut(self.config.n_layers)
+        use_swiftkv = (self.swiftkv.enabled and batch.kind is BatchKind.PREFILL
+                       and cut_full < self.config.n_layers)
+        if use_swiftkv and span_logits:
+            raise ContractViolation("span logits unsupported with early-exit prefill")
+        v = self.config.vocab_size
+        for it in batch.items:
+            for tok in it.tokens:
+                if not 0 <= tok < v:
+                    raise ContractViolation(f"token id {tok} outside vocab [0, {v})")
+        alloc = self.pool.alloc
+        need = sum(alloc.blocks_needed(it.seq.cache.key, it.seq.cache.token_count + len(it.tokens))
+                   for it in batch.items)
+        if need > alloc.free_blocks:
+            raise CacheOverflow(f"paged KV pool exhausted: {need} blocks needed, "
+                                f"{alloc.free_blocks} free")
+        for it in batch.items:
+            alloc.reserve(it.seq.cache.key, it.seq.cache.token_count + len(it.tokens))
+        meta = self._metadata(batch, mode, span_logits, cut_full if use_swiftkv else None)
+        self.group.begin_step(self._step_counter)
+        rec_start = len(self.group.records)
+        meters = [FlopMeter() for _ in range(self.world_size)]
+        cut = cut_full if use_swiftkv else None
+        if mode is ParallelMode.TP:
+            logits = self._forward_tp(meta, batch, meters, span_logits, cut)
+        else:
+            logits = self._forward_sp(meta, batch, meters, span_logits, cut)
+        for it in batch.items:
+            it.seq.cache.commit(len(it.tokens))
+        record = StepRecord(step_id=self._step_counter, mode=mode, kind=batch.kind,
+                            new_tokens=meta.M, n_requests=meta.n,
+                            flops_per_device=tuple(m.flops for m in meters),
+                            comm=self._comm_events(self.group.records[rec_start:]),
+                            host_ms=(time.perf_counter() - t_host) * 1e3)
+        self.mode_log.append(mode)
+        self.step_records.append(record)
+        self._step_counter += 1
+        return logits, record
+
+    def forward_tp(self, batch: Batch, span_logits: bool = False):
+        return self.step(batch, mode=ParallelMode.TP, span_logits=span_logits)
+
+    def forward_sp(self, batch: Batch, span_logits: bool = False):
+        return self.step(batch, mode=ParallelMode.SP, span_logits=span_logits)
+
+    def pass_shape(self, batch: Batch, span_logits: bool = False) -> PassShape:
+        return PassShape(spans=tuple(len(it.tokens) for it in batch.items),
+                         history=tuple(it.seq.cache.token_count for it in batch.items),
+                         span_logits=span_logits)
+
+    @staticmethod
+    def _comm_events(records: Seq[CommRecord]) -> Tuple[CommEvent, ...]:
+        by = {}
+        for r in records:
+            cur = by.get(r.event_id)
+            if cur is None or r.bytes > cur[1]:
+                by[r.event_id] = (r.kind, r.bytes)
+        return tuple(CommEvent(k, b) for k, b in (by[e] for e in sorted(by)))
+
+    # ----------------------------------------------------------- metadata
+    def _pinned_buffer(self, n: int) -> torch.Tensor:
+        if not self._pinned:
+            self._pinned = [torch.empty(0, dtype=torch.int32).pin_memory() for _ in range(2)]
+            self._pin_events = [None, None]
+        i = self._pin_idx
+        self._pin_idx ^= 1
+        ev = self._pin_events[i]
+        if ev is not None:
+            ev.synchronize()  # the previous copy out of this buffer has finished
+        if self._pinned[i].numel() < n:
+            self._pinned[i] = torch.empty(max(n, 2 * self._pinned[i].numel()),
+                                          dtype=torch.int32).pin_memory()
+        return self._pinned[i], i
+
+    def _metadata(self, batch: Batch, mode: ParallelMode, span_logits: bool,
+                  cut: Optional[int]) -> _Meta:
+        """Flatten the batch (parallel_engine.py:307-329) and build every index
+        array the kernels need; one pinned H2D copy."""
+        cfg = self.config
+        P = self.world_size
+        bs = self.pool.block_size
+        alloc = self.pool.alloc
+        items = batch.items
+        n = len(items)
+        spans = [len(it.tokens) for it in items]
+        hist = [it.seq.cache.token_count for it in items]
+        M = sum(spans)
+        toks = np.fromiter((t for it in items for t in it.tokens), dtype=np.int32, count=M)
+        pos = np.concatenate([np.arange(h0, h0 + m, dtype=np.int32) for h0, m in zip(hist, spans)])
+        slots = np.concatenate([alloc.slots(it.seq.cache.key, h0, m)
+                                for it, h0, m in zip(items, hist, spans)])
+        cu = np.zeros(n + 1, dtype=np.int32)
+        cu[1:] = np.cumsum(spans)
+        first = np.asarray(hist, dtype=np.int32)
+        kvlen = first + np.asarray(spans, dtype=np.int32)
+        width = max(len(alloc.tables[it.seq.cache.key]) for it in items)
+        bt = np.zeros((n, width), dtype=np.int32)
+        for i, it in enumerate(items):
+            tab = alloc.tables[it.seq.cache.key]
+            bt[i, :len(tab)] = tab
+        ends = (cu[1:] - 1).astype(np.int32)
+        decode_like = all(m == 1 for m in spans)
+        if decode_like:
+            work = np.zeros((0, 2), dtype=np.int32)
+        else:
+            tt = ops.attn_tile_tokens(cfg.n_heads // P, cfg.kv_heads // P)
+            wl = [(i, t0, hist[i] + t0) for i in range(n) for t0 in range(0, spans[i], tt)]
+            wl.sort(key=lambda w: -w[2])  # heaviest causal tiles first
+            work = np.asarray([(i, t0) for i, t0, _ in wl], dtype=np.int32).reshape(-1, 2)
+        bounds = shard_bounds(M, P)
+        # SP: per-rank local indices of the rows whose logits are returned
+        sp_rows = []
+        for lo, hi in bounds:
+            if span_logits:
+                sp_rows.append(np.arange(0, hi - lo, dtype=np.int32))
+            else:
+                sp_rows.append(np.asarray([e - lo for e in ends if lo <= e < hi], dtype=np.int32))
+        tail_pos = (kvlen - 1).astype(np.int32)
+        tail_slot = np.full(n, -1, dtype=np.int32)
+        tail_cu = np.arange(n + 1, dtype=np.int32)
+        parts = dict(toks=toks, pos=pos, slots=slots, cu=cu, first=first, kvlen=kvlen,
+                     bt=bt.reshape(-1), ends=ends, work=work.reshape(-1),
+                     tail_pos=tail_pos, tail_slot=tail_slot, tail_cu=tail_cu)
+        for r in range(P):
+            parts[f"sprows{r}"] = sp_rows[r]
+        # every array starts on a 16-byte boundary (the kernels read int2 pairs)
+        total = sum(-(-a.size // 4) * 4 for a in parts.values())
+        host, idx = self._pinned_buffer(total)
+        dev = torch.empty(max(total, 1), dtype=torch.int32, device=self.device)
+        views = {}
+        off = 0
+        hv = host.numpy()
+        for k, a in parts.items():
+            hv[off:off + a.size] = a
+            views[k] = (off, a.size)
+            off += -(-a.size // 4) * 4
+        dev[:total].copy_(host[:total], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._pin_events[idx] = ev
+        meta = _Meta()
+        for k, (o, s) in views.items():
+            setattr(meta, k, dev[o:o + s])
+        meta.bt = meta.bt.view(n, width)
+        meta.work_pairs = meta.work
+        meta.n_work = work.shape[0]
+        meta.M, meta.n, meta.spans, meta.hist = M, n, spans, hist
+        meta.ends_host = ends
+        meta.bounds = bounds
+        meta.rows = [hi - lo for lo, hi in bounds]
+        meta.sp_counts = [a.size for a in sp_rows]
+        meta.max_q = max(spans)
+        meta.max_kv = int(kvlen.max())
+        meta.windows = kvlen.tolist()
+        meta.decode_like = decode_like
+        self.last_slots = slots
+        self.last_block_table = bt
+        return meta
+
+    def _workspace(self, n_items: int, q_heads: int, max_kv: int) -> Optional[torch.Tensor]:
+        need = ops.attn_workspace_bytes(n_items, q_heads, self.config.head_dim, max_kv)
+        if self._ws is None or self._ws.numel() * 4 < need:
+            self._ws = torch.empty((need + 3) // 4, dtype=torch.float32, device=self.device)
+        return self._ws
+
+    # ------------------------------------------------------- shared pieces
+    def _attend(self, r: int, layer: int, q: torch.Tensor, out: torch.Tensor, meta: _Meta,
+                meter: FlopMeter, *, tails: bool = False) -> None:
+        cfg = self.config
+        P = self.world_size
+        hq, hk, d = cfg.n_heads // P, cfg.kv_heads // P, cfg.head_dim
+        if tails:
+            n_rows, cu, first = meta.n, meta.tail_cu, meta.tail_pos
+            decode_like = True
+            spans = [1] * meta.n
+        else:
+            n_rows, cu, first = meta.M, meta.cu, meta.first
+            decode_like = meta.decode_like
+            spans = meta.spans
+        ws = self._workspace(meta.n, hq, meta.max_kv) if decode_like else None
+        ops.attention(q, self.pool.layer_k(r, layer), self.pool.layer_v(r, layer), meta.bt, cu,
+                      first, meta.kvlen, out, n_items=meta.n,
+                      work=None if decode_like else meta.work_pairs,
+                      n_work=0 if decode_like else meta.n_work, max_q_len=max(spans),
+                      max_kv_len=meta.max_kv, q_heads=hq, kv_heads=hk, head_dim=d,
+                      block_size=self.pool.block_size, ws=ws)
+        # reference meter: per item per owned head, q·Kᵀ and P·V over the full window
+        for m, w in zip(spans, meta.windows):
+            meter.add_matmul(hq * m, d, w)
+            meter.add_matmul(hq * m, w, d)
+
+    def _kv_write(self, r: int, layer: int, qkv: torch.Tensor, q_out: Optional[torch.Tensor],
+                  meta: _Meta, batch: Batch, *, q_heads: Optional[int] = None,
+                  pos=None, slots=None, rows=None) -> None:
+        cfg = self.config
+        P = self.world_size
+        hq = cfg.n_heads // P if q_heads is None else q_heads
+        ops.rope_kv_write(qkv, meta.pos if pos is None else pos,
+                          meta.slots if slots is None else slots, self.weights.rope, q_out,
+                          self.pool.layer_k(r, layer), self.pool.layer_v(r, layer),
+                          rows=meta.M if rows is None else rows, q_heads=hq,
+                          kv_heads=cfg.kv_heads // P, head_dim=cfg.head_dim,
+                          block_size=self.pool.block_size)
+
+    def _stage_all(self, layer: int, batch: Batch) -> None:
+        # every process tracks the global cursors: all P devices append this layer
+        for it in batch.items:
+            for dev in range(self.world_size):
+                it.seq.cache._stage(dev, layer, len(it.tokens))
+
+    def _split(self, logits: torch.Tensor, meta: _Meta, span: bool) -> List[torch.Tensor]:
+        if span:
+            out, lo = [], 0
+            for m in meta.spans:
+                out.append(logits[lo:lo + m])
+                lo += m
+            return out
+        return [logits[i] for i in range(meta.n)]
+
+    # ================================================================= TP
+    def _forward_tp(self, meta, batch, meters, span_logits, cut):
+        cfg, w, g = self.config, self.weights, self.group
+        P = self.world_size
+        M, h, d = meta.M, cfg.hidden, cfg.head_dim
+        hq, hk = cfg.n_heads // P, cfg.kv_heads // P
+        W = w.qkv_width
+        hqw = hq * d
+        fl = cfg.ffn_dim // P
+        dev = self.device
+        eps = cfg.norm_eps
+        x = torch.empty((M, h), dtype=torch.float32, device=dev)
+        ops.embed(meta.toks, w.embed, x, meta.pos, w.pos_table)
+        pending: Optional[torch.Tensor] = None
+        n_full = cfg.n_layers if cut is None else cut
+        xn = torch.empty((M, h), dtype=torch.bfloat16, device=dev)
+        for layer in range(n_full):
+            lw = w.layers[layer]
+            ops.add_rmsnorm(x, lw.attn_gain, eps, xn, add=pending)
+            self._stage_all(layer, batch)
+            parts = {}
+            for r in g.local_ranks:
+                qkv = torch.empty((M, W), dtype=torch.bfloat16, device=dev)
+                ops.gemm(xn, lw.wqkv[r * W:(r + 1) * W], qkv, ops.EPI_STORE_BF16, M=M, N=W, K=h,
+                         lda=h, ldb=h, ldd=W, meter=meters[r])
+                q = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
+                self._kv_write(r, layer, qkv, q, meta, batch)
+                o = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
+                self._attend(r, layer, q, o, meta, meters[r])
+                wo = lw.wo[:, r * hqw:]
+                if P == 1:
+                    ops.gemm(o, wo, x, ops.EPI_ADD_F32, M=M, N=h, K=hqw, lda=hqw,
+                             ldb=cfg.n_heads * d, ldd=h, meter=meters[r])
+                else:
+                    part = torch.empty((M, h), dtype=torch.float32, device=dev)
+                    ops.gemm(o, wo, part, ops.EPI_STORE_F32, M=M, N=h, K=hqw, lda=hqw,
+                             ldb=cfg.n_heads * d, ldd=h, meter=meters[r])
+                    parts[r] = part
+            red = g.all_reduce_sum(parts)[g.local_ranks[0]] if P > 1 else None
+            xn2 = torch.empty((M, h), dtype=torch.bfloat16, device=dev)
+            ops.add_rmsnorm(x, lw.mlp_gain, eps, xn2, add=red)
+            parts = {}
+            for r in g.local_ranks:
+                act = torch.empty((M, fl), dtype=torch.bfloat16, device=dev)
+                self._mlp_up(xn2, lw, r, act, M, meters[r])
+                wd = lw.wdown[:, r * fl:]
+                if P == 1:
+                    ops.gemm(act, wd, x, ops.EPI_ADD_F32, M=M, N=h, K=fl, lda=fl,
+                             ldb=cfg.ffn_dim, ldd=h, meter=meters[r])
+                else:
+                    part = torch.empty((M, h), dtype=torch.float32, device=dev)
+                    ops.gemm(act, wd, part, ops.EPI_STORE_F32, M=M, N=h, K=fl, lda=fl,
+                             ldb=cfg.ffn_dim, ldd=h, meter=meters[r])
+                    parts[r] = part
+            pending = g.all_reduce_sum(parts)[g.local_ranks[0]] if P > 1 else None
+        if pending is not None:
+            ops.add_f32(x, pending, x)
+        if cut is not None:
+            x_rows, n_rows = self._tail_tp(meta, batch, meters, x, cut), meta.n
+            row_idx = None
+        else:
+            x_rows = x
+            if span_logits:
+                row_idx, n_rows = None, M
+            else:
+                row_idx, n_rows = meta.ends, meta.n
+        xf = torch.empty((n_rows, h), dtype=torch.bfloat16, device=dev)
+        ops.add_rmsnorm(x_rows, w.final_gain, eps, xf, row_idx=row_idx, rows=n_rows)
+        vs = cfg.vocab_size // P
+        parts = {}
+        for r in g.local_ranks:
+            lg = torch.empty((n_rows, vs), dtype=torch.float32, device=dev)
+            ops.gemm(xf, w.head[r * vs:(r + 1) * vs], lg, ops.EPI_STORE_F32, M=n_rows, N=vs, K=h,
+                     lda=h, ldb=h, ldd=vs, meter=meters[r])
+            parts[r] = lg
+        logits = self._gather_vocab(parts, n_rows)
+        return self._split(logits, meta, span_logits and cut is None)
+
+    def _mlp_up(self, xn2, lw, r, act, rows, meter):
+        cfg = self.config
+        P = self.world_size
+        h = cfg.hidden
+        fl = cfg.ffn_dim // P
+        if cfg.mlp == "swiglu":
+            ops.gemm(xn2, lw.wgu[r * 2 * fl:(r + 1) * 2 * fl], act, ops.EPI_SWIGLU, M=rows,
+                     N=2 * fl, K=h, lda=h, ldb=h, ldd=fl, meter=meter)
+        else:
+            ops.gemm(xn2, lw.wgu[r * fl:(r + 1) * fl], act, ops.EPI_GELU, M=rows, N=fl, K=h,
+                     lda=h, ldb=h, ldd=fl, meter=meter)
+
+    def _gather_vocab(self, parts: Dict[int, torch.Tensor], n_rows: int) -> torch.Tensor:
+        """TP logits all-gather (:392-398): per-rank [R, V/P] -> [R, V]."""
+        g = self.group
+        P = self.world_size
+        if P == 1:
+            return parts[0]
+        stacked = {r: t.t().contiguous() for r, t in parts.items()}  # [V/P, R] like head_rank
+        vs = self.config.vocab_size // P
+        full = g.all_gather_rows(stacked, [vs] * P)               # [V, R]
+        return full.t().contiguous()
+
+    def _tail_tp(self, meta, batch, meters, x, cut):
+        """SwiftKV TP tail (:400-450): later-layer K/V from z = norm(x, gain_cut),
+        then only each request's last row through layers >= cut."""
+        cfg, w, g = self.config, self.weights, self.group
+        P = self.world_size
+        M, h, d = meta.M, cfg.hidden, cfg.head_dim
+        hq, hk = cfg.n_heads // P, cfg.kv_heads // P
+        hqw, kvw = hq * d, 2 * hk * d
+        W = w.qkv_width
+        fl = cfg.ffn_dim // P
+        dev, eps = self.device, cfg.norm_eps
+        z = torch.empty((M, h), dtype=torch.bfloat16, device=dev)
+        ops.add_rmsnorm(x, w.layers[cut].attn_gain, eps, z)
+        for layer in range(cut, cfg.n_layers):
+            lw = w.layers[layer]
+            self._stage_all(layer, batch)
+            for r in g.local_ranks:
+                kv = torch.empty((M, kvw), dtype=torch.bfloat16, device=dev)
+                ops.gemm(z, lw.wkv[r * kvw:(r + 1) * kvw], kv, ops.EPI_STORE_BF16, M=M, N=kvw,
+                         K=h, lda=h, ldb=h, ldd=kvw, meter=meters[r])
+                self._kv_write(r, layer, kv, None, meta, batch, q_heads=0)
+        n = meta.n
+        xt = torch.empty((n, h), dtype=torch.float32, device=dev)
+        ops.gather_rows(x, meta.ends, xt)
+        xn = torch.empty((n, h), dtype=torch.bfloat16, device=dev)
+        pending = None
+        for layer in range(cut, cfg.n_layers):
+            lw = w.layers[layer]
+            ops.add_rmsnorm(xt, lw.attn_gain, eps, xn, add=pending)
+            parts = {}
+            for r in g.local_ranks:
+                qr = torch.empty((n, hqw), dtype=torch.bfloat16, device=dev)
+                ops.gemm(xn, lw.wqkv[r * W:r * W + hqw], qr, ops.EPI_STORE_BF16, M=n, N=hqw, K=h,
+                         lda=h, ldb=h, ldd=hqw, meter=meters[r])
+                q = torch.empty((n, hqw), dtype=torch.bfloat16, device=dev)
+                ops.rope_kv_write(qr, meta.tail_pos, meta.tail_slot, w.rope, q,
+                                  self.pool.layer_k(r, layer), self.pool.layer_v(r, layer),
+                                  rows=n, q_heads=hq, kv_heads=0, head_dim=d,
+                                  block_size=self.pool.block_size)
+                o = torch.empty((n, hqw), dtype=torch.bfloat16, device=dev)
+                self._attend(r, layer, q, o, meta, meters[r], tails=True)
+                wo = lw.wo[:, r * hqw:]
+                if P == 1:
+                    ops.gemm(o, wo, xt, ops.EPI_ADD_F32, M=n, N=h, K=hqw, lda=hqw,
+                             ldb=cfg.n_heads * d, ldd=h, meter=meters[r])
+                else:
+                    part = torch.empty((n, h), dtype=torch.float32, device=dev)
+                    ops.gemm(o, wo, part, ops.EPI_STORE_F32, M=n, N=h, K=hqw, lda=hqw,
+                             ldb=cfg.n_heads * d, ldd=h, meter=meters[r])
+                    parts[r] = part
+            red = g.all_reduce_sum(parts)[g.local_ranks[0]] if P > 1 else None
+            xn2 = torch.empty((n, h), dtype=torch.bfloat16, device=dev)
+            ops.add_rmsnorm(xt, lw.mlp_gain, eps, xn2, add=red)
+            parts = {}
+            for r in g.local_ranks:
+                act = torch.empty((n, fl), dtype=torch.bfloat16, device=dev)
+                self._mlp_up(xn2, lw, r, act, n, meters[r])
+                wd = lw.wdown[:, r * fl:]
+                if P == 1:
+                    ops.gemm(act, wd, xt, ops.EPI_ADD_F32, M=n, N=h, K=fl, lda=fl,
+                             ldb=cfg.ffn_dim, ldd=h, meter=meters[r])
+                else:
+                    part = torch.empty((n, h), dtype=torch.float32, device=dev)
+                    ops.gemm(act, wd, part, ops.EPI_STORE_F32, M=n, N=h, K=fl, lda=fl,
+                             ldb=cfg.ffn_dim, ldd=h, meter=meters[r])
+                    parts[r] = part
+            pending = g.all_reduce_sum(parts)[g.local_ranks[0]] if P > 1 else None
+        if pending is not None:
+            ops.add_f32(xt, pending, xt)
+        return xt
+
+    # ================================================================= SP
+    def _forward_sp(self, meta, batch, meters, span_logits, cut):
+        cfg, w, g = self.config, self.weights, self.group
+        P = self.world_size
+        M, h, d = meta.M, cfg.hidden, cfg.head_dim
+        hq = cfg.n_heads // P
+        W = w.qkv_width
+        hqw = hq * d
+        dev, eps = self.device, cfg.norm_eps
+        rows, bounds = meta.rows, meta.bounds
+        xs = {}
+        for r in g.local_ranks:
+            lo, hi = bounds[r]
+            xs[r] = torch.empty((hi - lo, h), dtype=torch.float32, device=dev)
+            ops.embed(meta.toks[lo:hi], w.embed, xs[r], meta.pos[lo:hi], w.pos_table)
+        n_full = cfg.n_layers if cut is None else cut
+        in_fwd = {r: [rows[r]] * P for r in range(P)}
+        out_fwd = {s: list(rows) for s in range(P)}
+        for layer in range(n_full):
+            lw = w.layers[layer]
+            send, recv = {}, {}
+            for r in g.local_ranks:
+                xn = torch.empty((rows[r], h), dtype=torch.bfloat16, device=dev)
+                ops.add_rmsnorm(xs[r], lw.attn_gain, eps, xn)
+                if P == 1:
+                    send[r] = torch.empty((M, W), dtype=torch.bfloat16, device=dev)
+                    ops.gemm(xn, lw.wqkv, send[r], ops.EPI_STORE_BF16, M=M, N=W, K=h, lda=h,
+                             ldb=h, ldd=W, meter=meters[r])
+                    recv[r] = send[r]
+                else:
+                    # epilogue writes rank s's q|k|v heads into send block s (fused pack)
+                    send[r] = torch.empty((P * rows[r], W), dtype=torch.bfloat16, device=dev)
+                    ops.gemm(xn, lw.wqkv, send[r], ops.EPI_STORE_BF16, M=rows[r], N=P * W, K=h,
+                             lda=h, ldb=h, ldd=W, peer_width=W, peer_stride=rows[r] * W,
+                             meter=meters[r])
+                    recv[r] = torch.empty((M, W), dtype=torch.bfloat16, device=dev)
+            if P > 1:
+                g.all_to_all(send, recv, in_fwd, out_fwd, row_bytes=W * 2)
+            self._stage_all(layer, batch)
+            att = {}
+            for r in g.local_ranks:
+                q = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
+                self._kv_write(r, layer, recv[r], q, meta, batch)
+                o = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
+                self._attend(r, layer, q, o, meta, meters[r])
+                att[r] = o
+            back = att
+            if P > 1:
+                back = {r: torch.empty((P * rows[r], hqw), dtype=torch.bfloat16, device=dev)
+                        for r in g.local_ranks}
+                g.all_to_all(att, back, {r: list(rows) for r in range(P)},
+                             {s: [rows[s]] * P for s in range(P)}, row_bytes=hqw * 2)
+            for r in g.local_ranks:
+                self._o_proj_sp(back[r], lw, xs[r], rows[r], meters[r])
+                xn2 = torch.empty((rows[r], h), dtype=torch.bfloat16, device=dev)
+                ops.add_rmsnorm(xs[r], lw.mlp_gain, eps, xn2)
+                act = torch.empty((rows[r], cfg.ffn_dim), dtype=torch.bfloat16, device=dev)
+                self._mlp_up_full(xn2, lw, act, rows[r], meters[r])
+                ops.gemm(act, lw.wdown, xs[r], ops.EPI_ADD_F32, M=rows[r], N=h, K=cfg.ffn_dim,
+                         lda=cfg.ffn_dim, ldb=cfg.ffn_dim, ldd=h, meter=meters[r])
+        if cut is not None:
+            return self._tail_sp(meta, batch, meters, xs, cut)
+        parts = {}
+        for r in g.local_ranks:
+            cnt = meta.sp_counts[r]
+            xf = torch.empty((cnt, h), dtype=torch.bfloat16, device=dev)
+            idx = getattr(meta, f"sprows{r}")
+            ops.add_rmsnorm(xs[r], w.final_gain, eps, xf, row_idx=idx, rows=cnt)
+            lg = torch.empty((cnt, cfg.vocab_size), dtype=torch.float32, device=dev)
+            ops.gemm(xf, w.head, lg, ops.EPI_STORE_F32, M=cnt, N=cfg.vocab_size, K=h, lda=h,
+                     ldb=h, ldd=cfg.vocab_size, meter=meters[r])
+            parts[r] = lg
+        logits = g.all_gather_rows(parts, meta.sp_counts) if P > 1 else parts[0]
+        return self._split(logits, meta, span_logits)
+
+    def _mlp_up_full(self, xn2, lw, act, rows, meter):
+        cfg = self.config
+        h, f = cfg.hidden, cfg.ffn_dim
+        if cfg.mlp == "swiglu":
+            ops.gemm(xn2, lw.wgu, act, ops.EPI_SWIGLU, M=rows, N=2 * f, K=h, lda=h, ldb=h, ldd=f,
+                     meter=meter)
+        else:
+            ops.gemm(xn2, lw.wgu, act, ops.EPI_GELU, M=rows, N=f, K=h, lda=h, ldb=h, ldd=f,
+                     meter=meter)
+
+    def _o_proj_sp(self, back: torch.Tensor, lw, x: torch.Tensor, rows: int, meter) -> None:
+        """x += back · Wo^T where back is [P][rows][Hq/P·d] (all-to-all receive)."""
+        cfg = self.config
+        P = self.world_size
+        hqw = cfg.n_heads // P * cfg.head_dim
+        K = cfg.n_heads * cfg.head_dim
+        if P == 1:
+            ops.gemm(back, lw.wo, x, ops.EPI_ADD_F32, M=rows, N=cfg.hidden, K=K, lda=K, ldb=K,
+                     ldd=cfg.hidden, meter=meter)
+        elif hqw % 64 == 0:
+            ops.gemm(back, lw.wo, x, ops.EPI_ADD_F32, M=rows, N=cfg.hidden, K=K, lda=hqw, ldb=K,
+                     ldd=cfg.hidden, a_kchunk=hqw, a_chunk_stride=rows * hqw, meter=meter)
+        else:
+            flat = torch.empty((rows, K), dtype=torch.bfloat16, device=x.device)
+            ops.a2a_unpack(back, flat, rows, P, hqw)
+            ops.gemm(flat, lw.wo, x, ops.EPI_ADD_F32, M=rows, N=cfg.hidden, K=K, lda=K, ldb=K,
+                     ldd=cfg.hidden, meter=meter)
+
+    def _tail_sp(self, meta, batch, meters, xs, cut):
+        """SwiftKV SP tail (:544-647): K/V for layers >= cut projected token-locally
+        from z = norm(x, gain_cut) and re-sharded by all-to-all; each request's
+        last row stays on the rank that owns it."""
+        cfg, w, g = self.config, self.weights, self.group
+        P = self.world_size
+        M, h, d = meta.M, cfg.hidden, cfg.head_dim
+        hq, hk = cfg.n_heads // P, cfg.kv_heads // P
+        hqw, kvw = hq * d, 2 * hk * d
+        W = w.qkv_width
+        dev, eps = self.device, cfg.norm_eps
+        rows, bounds = meta.rows, meta.bounds
+        zs = {}
+        for r in g.local_ranks:
+            zs[r] = torch.empty((rows[r], h), dtype=torch.bfloat16, device=dev)
+            ops.add_rmsnorm(xs[r], w.layers[cut].attn_gain, eps, zs[r])
+        in_fwd = {r: [rows[r]] * P for r in range(P)}
+        out_fwd = {s: list(rows) for s in range(P)}
+        for layer in range(cut, cfg.n_layers):
+            lw = w.layers[layer]
+            send, recv = {}, {}
+            for r in g.local_ranks:
+                if P == 1:
+                    send[r] = torch.empty((M, kvw), dtype=torch.bfloat16, device=dev)
+                    ops.gemm(zs[r], lw.wkv, send[r], ops.EPI_STORE_BF16, M=M, N=kvw, K=h, lda=h,
+                             ldb=h, ldd=kvw, meter=meters[r])
+                    recv[r] = send[r]
+                else:
+                    send[r] = torch.empty((P * rows[r], kvw), dtype=torch.bfloat16, device=dev)
+                    ops.gemm(zs[r], lw.wkv, send[r], ops.EPI_STORE_BF16, M=rows[r], N=P * kvw,
+                             K=h, lda=h, ldb=h, ldd=kvw, peer_width=kvw,
+                             peer_stride=rows[r] * kvw, meter=meters[r])
+                    recv[r] = torch.empty((M, kvw), dtype=torch.bfloat16, device=dev)
+            if P > 1:
+                g.all_to_all(send, recv, in_fwd, out_fwd, row_bytes=kvw * 2)
+            self._stage_all(layer, batch)
+            for r in g.local_ranks:
+                self._kv_write(r, layer, recv[r], None, meta, batch, q_heads=0)
+        # tails: last row of each request, on its owner rank (ends are ordered by rank)
+        ends = meta.ends_host
+        owned = [[int(e - lo) for e in ends if lo <= e < hi] for lo, hi in bounds]
+        cnt = [len(o) for o in owned]
+        tails, tpos, tslot = {}, {}, {}
+        first_end = np.cumsum([0] + cnt)
+        for r in g.local_ranks:
+            idx = torch.as_tensor(np.asarray(owned[r], dtype=np.int32), device=dev)
+            tails[r] = torch.empty((cnt[r], h), dtype=torch.float32, device=dev)
+            ops.gather_rows(xs[r], idx, tails[r])
+        tpos_all = meta.tail_pos
+        n = meta.n
+        for layer in range(cut, cfg.n_layers):
+            lw = w.layers[layer]
+            send, recv = {}, {}
+            for r in g.local_ranks:
+                xn = torch.empty((cnt[r], h), dtype=torch.bfloat16, device=dev)
+                ops.add_rmsnorm(tails[r], lw.attn_gain, eps, xn)
+                send[r] = torch.empty((P * cnt[r], hqw), dtype=torch.bfloat16, device=dev)
+                for s in range(P):  # q heads of peer s (rows [sW, sW + hq d) of wqkv)
+                    ops.gemm(xn, lw.wqkv[s * W:s * W + hqw], send[r][s * cnt[r]:], ops.EPI_STORE_BF16,
+                             M=cnt[r], N=hqw, K=h, lda=h, ldb=h, ldd=hqw, meter=meters[r])
+                recv[r] = send[r] if P == 1 else torch.empty((n, hqw), dtype=torch.bfloat16,
+                                                             device=dev)
+            if P > 1:
+                g.all_to_all(send, recv, {r: [cnt[r]] * P for r in range(P)},
+                             {s: list(cnt) for s in range(P)}, row_bytes=hqw * 2)
+            att = {}
+            for r in g.local_ranks:
+                q = torch.empty((n, hqw), dtype=torch.bfloat16, device=dev)
+                ops.rope_kv_write(recv[r], tpos_all, meta.tail_slot, w.rope, q,
+                                  self.pool.layer_k(r, layer), self.pool.layer_v(r, layer),
+                                  rows=n, q_heads=hq, kv_heads=0, head_dim=d,
+                                  block_size=self.pool.block_size)
+                o = torch.empty((n, hqw), dtype=torch.bfloat16, device=dev)
+                self._attend(r, layer, q, o, meta, meters[r], tails=True)
+                att[r] = o
+            back = att
+            if P > 1:
+                back = {r: torch.empty((P * cnt[r], hqw), dtype=torch.bfloat16, device=dev)
+                        for r in g.local_ranks}
+                g.all_to_all(att, back, {r: list(cnt) for r in range(P)},
+                             {s: [cnt[s]] * P for s in range(P)}, row_bytes=hqw * 2)
+            for r in g.local_ranks:
+                self._o_proj_sp(back[r], lw, tails[r], cnt[r], meters[r])
+                xn2 = torch.empty((cnt[r], h), dtype=torch.bfloat16, device=dev)
+                ops.add_rmsnorm(tails[r], lw.mlp_gain, eps, xn2)
+                act = torch.empty((cnt[r], cfg.ffn_dim), dtype=torch.bfloat16, device=dev)
+                self._mlp_up_full(xn2, lw, act, cnt[r], meters[r])
+                ops.gemm(act, lw.wdown, tails[r], ops.EPI_ADD_F32, M=cnt[r], N=h, K=cfg.ffn_dim,
+                         lda=cfg.ffn_dim, ldb=cfg.ffn_dim, ldd=h, meter=meters[r])
+        parts = {}
+        for r in g.local_ranks:
+            xf = torch.empty((cnt[r], h), dtype=torch.bfloat16, device=dev)
+            ops.add_rmsnorm(tails[r], w.final_gain, eps, xf)
+            lg = torch.empty((cnt[r], cfg.vocab_size), dtype=torch.float32, device=dev)
+            ops.gemm(xf, w.head, lg, ops.EPI_STORE_F32, M=cnt[r], N=cfg.vocab_size, K=h, lda=h,
+                     ldb=h, ldd=cfg.vocab_size, meter=meters[r])
+            parts[r] = lg
+        logits = g.all_gather_rows(parts, cnt) if P > 1 else parts[0]
+        # gathered rows are in rank order == item order (ends increase with rank)
+        return [logits[i] for i in range(n)]
+
+
+def greedy_tokens(logits: List[torch.Tensor]) -> List[int]:
+    """greedy_token (model.py:303-307) for every item: one argmax kernel, one D2H."""
+    if not logits:
+        return []
+    rows = torch.stack([l if l.dim() == 1 else l[-1] for l in logits])
+    idx = torch.empty(rows.shape[0], dtype=torch.int32, device=rows.device)
+    ops.argmax(rows, idx)
+    return idx.cpu().tolist()

@@ -1,0 +1,191 @@
+"""Device groups: the collectives of the Shift-Parallel path.
+
+Mirrors ``DeviceGroup`` (/root/reference/pkg/src/shiftsim/fabric.py:54-228):
+rank-ordered all-to-all with uneven row counts (:145-171), all-reduce-sum
+(:117-143), rank-ordered all-gather (:173-191), plus the reference's
+ring-model byte ledger (:10-15) so step records compare one-to-one.
+
+Two implementations behind one interface (bulk-synchronous over the ranks a
+process drives, like ``map_ranks`` :72-80):
+
+* ``NcclGroup`` — production: one process per GPU (torchrun), torch.distributed
+  over NCCL on NVLink/NVSwitch; this process drives exactly its own rank.
+* ``LoopbackGroup`` — P simulated ranks on ONE device in one process (the
+  reference's own execution model); collectives are device-to-device copies
+  and an ascending-rank f32 sum kernel.  Used by the single-GPU parity tests
+  (SP/TP at P = 2, 4 on one B200) and by the CPU gloo tests of the host logic.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence
+
+import torch
+
+from .errors import ContractViolation
+
+
+@dataclass(frozen=True)
+class CommRecord:
+    kind: str
+    device: int
+    bytes: float
+    step_id: int
+    event_id: int
+
+
+class _Ledger:
+    def __init__(self, world_size: int):
+        self.world_size = world_size
+        self.records: List[CommRecord] = []
+        self.step_id = 0
+        self._events = 0
+
+    def begin_step(self, step_id: int) -> None:
+        self.step_id = step_id
+
+    def charge(self, kind: str, per_device: Sequence[float]) -> None:
+        ev = self._events
+        self._events += 1
+        for d, b in enumerate(per_device):
+            self.records.append(CommRecord(kind, d, float(b), self.step_id, ev))
+
+    def device_bytes(self, device: int) -> float:
+        return sum(r.bytes for r in self.records if r.device == device)
+
+    def ledger(self) -> Dict[int, Dict[str, float]]:
+        out: Dict[int, Dict[str, float]] = {d: {} for d in range(self.world_size)}
+        for r in self.records:
+            out[r.device][r.kind] = out[r.device].get(r.kind, 0.0) + r.bytes
+        return out
+
+    def reset_ledger(self) -> None:
+        self.records = []
+        self._events = 0
+
+
+class DeviceGroup(_Ledger):
+    """Interface shared by the NCCL and loopback groups."""
+
+    world_size: int
+    local_ranks: List[int]
+    device: torch.device
+
+    # byte accounting from the global split tables (every rank knows them)
+    def _charge_a2a(self, in_splits: Dict[int, List[int]], row_bytes: int) -> None:
+        p = self.world_size
+        self.charge("all_to_all", [(p - 1) / p * sum(in_splits[r]) * row_bytes for r in range(p)])
+
+    def all_to_all(self, send, recv, in_splits, out_splits, row_bytes):  # pragma: no cover
+        raise NotImplementedError
+
+    def all_reduce_sum(self, parts: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:  # pragma: no cover
+        raise NotImplementedError
+
+    def all_gather_rows(self, parts: Dict[int, torch.Tensor], counts: List[int]) -> torch.Tensor:  # pragma: no cover
+        raise NotImplementedError
+
+    def barrier(self) -> None:
+        pass
+
+
+class LoopbackGroup(DeviceGroup):
+    """P ranks simulated on one device (reference execution model)."""
+
+    def __init__(self, world_size: int, device="cuda"):
+        if world_size < 1:
+            raise ContractViolation("world_size must be >= 1")
+        super().__init__(world_size)
+        self.local_ranks = list(range(world_size))
+        self.device = torch.device(device)
+        self._add = None  # set by the engine to the sp_add_f32 kernel wrapper
+
+    def all_to_all(self, send: Dict[int, torch.Tensor], recv: Dict[int, torch.Tensor],
+                   in_splits: Dict[int, List[int]], out_splits: Dict[int, List[int]],
+                   row_bytes: int) -> None:
+        """Rank r sends rows in_splits[r][s] of send[r] (in peer order) to s;
+        rank s receives them at recv[s] in source order (fabric.py:145-171)."""
+        p = self.world_size
+        offs_in = {r: [sum(in_splits[r][:s]) for s in range(p)] for r in range(p)}
+        for s in range(p):
+            off = 0
+            for r in range(p):
+                n = in_splits[r][s]
+                if n != out_splits[s][r]:
+                    raise ContractViolation("all_to_all split tables disagree")
+                if n:
+                    recv[s][off:off + n].copy_(send[r][offs_in[r][s]:offs_in[r][s] + n])
+                off += n
+        self._charge_a2a(in_splits, row_bytes)
+
+    def all_reduce_sum(self, parts: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:
+        """Ascending-rank f32 sum; every rank gets the same (aliased) result."""
+        p = self.world_size
+        total = parts[0]
+        if p > 1:
+            total = parts[0].clone()
+            for r in range(1, p):
+                if self._add is None:
+                    raise ContractViolation("loopback all-reduce needs the engine's add kernel")
+                self._add(total, parts[r], total)
+        self.charge("all_reduce", [2.0 * (p - 1) / p * parts[0].numel() * parts[0].element_size()] * p)
+        return {r: total for r in range(p)}
+
+    def all_gather_rows(self, parts: Dict[int, torch.Tensor], counts: List[int]) -> torch.Tensor:
+        p = self.world_size
+        full = torch.cat([parts[r][:counts[r]] for r in range(p)], dim=0)
+        self.charge("all_gather", [(p - 1) / p * full.numel() * full.element_size()] * p)
+        return full
+
+
+class NcclGroup(DeviceGroup):
+    """One rank per process over torch.distributed (NCCL on B200, gloo on CPU tests)."""
+
+    def __init__(self, device=None):
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            raise ContractViolation("torch.distributed must be initialised before NcclGroup")
+        super().__init__(dist.get_world_size())
+        self.rank = dist.get_rank()
+        self.local_ranks = [self.rank]
+        self.device = torch.device(device) if device is not None else (
+            torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
+            else torch.device("cpu"))
+        self._dist = dist
+
+    def all_to_all(self, send, recv, in_splits, out_splits, row_bytes) -> None:
+        me = self.rank
+        if self.world_size > 1:
+            self._dist.all_to_all_single(recv[me], send[me], output_split_sizes=out_splits[me],
+                                         input_split_sizes=in_splits[me])
+        self._charge_a2a(in_splits, row_bytes)
+
+    def all_reduce_sum(self, parts):
+        me, p = self.rank, self.world_size
+        t = parts[me]
+        if p > 1:
+            self._dist.all_reduce(t)
+        self.charge("all_reduce", [2.0 * (p - 1) / p * t.numel() * t.element_size()] * p)
+        return {me: t}
+
+    def all_gather_rows(self, parts, counts) -> torch.Tensor:
+        me, p = self.rank, self.world_size
+        t = parts[me]
+        width = t.shape[1]
+        mx = max(counts) if counts else 0
+        if p == 1:
+            full = t[:counts[0]]
+        else:
+            pad = torch.zeros((mx, width), dtype=t.dtype, device=t.device)
+            pad[:counts[me]].copy_(t[:counts[me]])
+            buf = torch.empty((p * mx, width), dtype=t.dtype, device=t.device)
+            self._dist.all_gather_into_tensor(buf, pad)
+            full = torch.cat([buf[r * mx:r * mx + counts[r]] for r in range(p)], dim=0)
+        nbytes = sum(counts) * width * t.element_size()
+        self.charge("all_gather", [(p - 1) / p * nbytes] * p)
+        return full
+
+    def barrier(self) -> None:
+        if self.world_size > 1:
+            self._dist.barrier()

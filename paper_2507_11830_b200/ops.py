@@ -1,0 +1,196 @@
+"""Typed wrappers over the C-ABI (include/shiftpar.h) for torch CUDA tensors.
+
+Every wrapper validates its operands, forwards raw device pointers and the
+current CUDA stream to libshiftpar.so, and maps a nonzero status to
+``ContractViolation``.  ``launch_count`` counts the kernels enqueued (the
+``gpu_launches`` figure of bench.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import torch
+
+from . import _lib
+from .errors import ContractViolation
+
+EPI_STORE_BF16 = 0
+EPI_STORE_F32 = 1
+EPI_ADD_F32 = 2
+EPI_SWIGLU = 3
+EPI_GELU = 4
+
+launch_count = 0
+
+
+def _count(n: int = 1) -> None:
+    global launch_count
+    launch_count += n
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _need(t: torch.Tensor, dtype: torch.dtype, what: str) -> None:
+    if not t.is_cuda:
+        raise ContractViolation(f"{what}: tensor must live on the GPU")
+    if t.dtype != dtype:
+        raise ContractViolation(f"{what}: want {dtype}, got {t.dtype}")
+
+
+def device_check() -> int:
+    lib = _lib.load()
+    n = ctypes.c_int(0)
+    _lib.check(lib.sp_device_check(ctypes.byref(n)), "sp_device_check")
+    return n.value
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, epilogue: int, *, M: int, N: int,
+         K: int, lda: int, ldb: int, ldd: int, a_kchunk: int = 0, a_chunk_stride: int = 0,
+         peer_width: int = 0, peer_stride: int = 0, meter=None) -> None:
+    """D = epi(A[M,K] B[N,K]^T) — see sp_gemm_bf16.  A/B may be views with
+    arbitrary base offsets (zero-copy TP shards)."""
+    _need(a, torch.bfloat16, "gemm A")
+    _need(b, torch.bfloat16, "gemm B")
+    if epilogue in (EPI_STORE_BF16, EPI_SWIGLU, EPI_GELU):
+        _need(d, torch.bfloat16, "gemm D")
+    else:
+        _need(d, torch.float32, "gemm D")
+    if meter is not None:
+        meter.add_matmul(M, K, N)
+    if M == 0:
+        return
+    lib = _lib.load()
+    rc = lib.sp_gemm_bf16(a.data_ptr(), lda, a_kchunk, a_chunk_stride, b.data_ptr(), ldb,
+                          d.data_ptr(), ldd, M, N, K, epilogue, peer_width, peer_stride, _stream())
+    _lib.check(rc, "sp_gemm_bf16")
+    _count()
+
+
+def embed(ids: torch.Tensor, table: torch.Tensor, out: torch.Tensor,
+          pos: Optional[torch.Tensor] = None, pos_table: Optional[torch.Tensor] = None) -> None:
+    _need(ids, torch.int32, "embed ids")
+    _need(table, torch.bfloat16, "embed table")
+    _need(out, torch.float32, "embed out")
+    rows = ids.shape[0]
+    if rows == 0:
+        return
+    rc = _lib.load().sp_embed(ids.data_ptr(), table.data_ptr(), _ptr(pos), _ptr(pos_table),
+                              out.data_ptr(), rows, table.shape[1], _stream())
+    _lib.check(rc, "sp_embed")
+    _count()
+
+
+def add_rmsnorm(x: torch.Tensor, gain: torch.Tensor, eps: float, out: torch.Tensor, *,
+                add: Optional[torch.Tensor] = None, row_idx: Optional[torch.Tensor] = None,
+                rows: Optional[int] = None) -> None:
+    _need(x, torch.float32, "rmsnorm x")
+    _need(gain, torch.float32, "rmsnorm gain")
+    _need(out, torch.bfloat16, "rmsnorm out")
+    n = (row_idx.shape[0] if row_idx is not None else x.shape[0]) if rows is None else rows
+    if n == 0:
+        return
+    h = x.shape[1]
+    rc = _lib.load().sp_add_rmsnorm(x.data_ptr(), x.stride(0), _ptr(add), gain.data_ptr(),
+                                    float(eps), _ptr(row_idx), out.data_ptr(), out.stride(0), n, h,
+                                    _stream())
+    _lib.check(rc, "sp_add_rmsnorm")
+    _count()
+
+
+def rope_kv_write(qkv: torch.Tensor, pos: torch.Tensor, slot: torch.Tensor,
+                  rope: Optional[torch.Tensor], q_out: Optional[torch.Tensor],
+                  k_pool: torch.Tensor, v_pool: torch.Tensor, *, rows: int, q_heads: int,
+                  kv_heads: int, head_dim: int, block_size: int) -> None:
+    _need(qkv, torch.bfloat16, "rope qkv")
+    if rows == 0:
+        return
+    rc = _lib.load().sp_rope_kv_write(qkv.data_ptr(), qkv.stride(0), pos.data_ptr(),
+                                      slot.data_ptr(), _ptr(rope), _ptr(q_out),
+                                      0 if q_out is None else q_out.stride(0),
+                                      k_pool.data_ptr(), v_pool.data_ptr(), rows, q_heads,
+                                      kv_heads, head_dim, block_size, _stream())
+    _lib.check(rc, "sp_rope_kv_write")
+    _count()
+
+
+def attn_tile_tokens(q_heads: int, kv_heads: int) -> int:
+    return _lib.load().sp_attn_tile_tokens(q_heads, kv_heads)
+
+
+def attn_workspace_bytes(n_items: int, q_heads: int, head_dim: int, max_kv: int) -> int:
+    return _lib.load().sp_attn_workspace_bytes(n_items, q_heads, head_dim, max_kv)
+
+
+def attention(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
+              block_tables: torch.Tensor, cu_q: torch.Tensor, first_pos: torch.Tensor,
+              kv_len: torch.Tensor, out: torch.Tensor, *, n_items: int,
+              work: Optional[torch.Tensor], n_work: int, max_q_len: int, max_kv_len: int,
+              q_heads: int, kv_heads: int, head_dim: int, block_size: int,
+              ws: Optional[torch.Tensor]) -> None:
+    _need(q, torch.bfloat16, "attention q")
+    _need(out, torch.bfloat16, "attention out")
+    if n_items == 0:
+        return
+    ws_bytes = 0 if ws is None else ws.numel() * ws.element_size()
+    rc = _lib.load().sp_attention(q.data_ptr(), q.stride(0), k_pool.data_ptr(), v_pool.data_ptr(),
+                                  block_tables.data_ptr(), block_tables.stride(0), cu_q.data_ptr(),
+                                  first_pos.data_ptr(), kv_len.data_ptr(), n_items, _ptr(work),
+                                  n_work, max_q_len, max_kv_len, out.data_ptr(), out.stride(0),
+                                  q_heads, kv_heads, head_dim, block_size, _ptr(ws), ws_bytes,
+                                  _stream())
+    _lib.check(rc, "sp_attention")
+    _count(1 if n_work > 0 else 2)
+
+
+def a2a_pack(src: torch.Tensor, dst: torch.Tensor, rows: int, peers: int, width: int) -> None:
+    if rows == 0:
+        return
+    _lib.check(_lib.load().sp_a2a_pack(src.data_ptr(), src.stride(0), dst.data_ptr(), rows, peers,
+                                       width, _stream()), "sp_a2a_pack")
+    _count()
+
+
+def a2a_unpack(src: torch.Tensor, dst: torch.Tensor, rows: int, peers: int, width: int) -> None:
+    if rows == 0:
+        return
+    _lib.check(_lib.load().sp_a2a_unpack(src.data_ptr(), dst.data_ptr(), dst.stride(0), rows,
+                                         peers, width, _stream()), "sp_a2a_unpack")
+    _count()
+
+
+def add_f32(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor) -> None:
+    _need(a, torch.float32, "add a")
+    n = a.numel()
+    if n == 0:
+        return
+    _lib.check(_lib.load().sp_add_f32(a.data_ptr(), b.data_ptr(), out.data_ptr(), n, _stream()),
+               "sp_add_f32")
+    _count()
+
+
+def argmax(logits: torch.Tensor, idx: torch.Tensor, val: Optional[torch.Tensor] = None) -> None:
+    _need(logits, torch.float32, "argmax logits")
+    rows, vocab = logits.shape
+    if rows == 0:
+        return
+    _lib.check(_lib.load().sp_argmax(logits.data_ptr(), logits.stride(0), rows, vocab,
+                                     idx.data_ptr(), _ptr(val), _stream()), "sp_argmax")
+    _count()
+
+
+def gather_rows(src: torch.Tensor, idx: torch.Tensor, dst: torch.Tensor) -> None:
+    rows = idx.shape[0]
+    if rows == 0:
+        return
+    _lib.check(_lib.load().sp_gather_rows_f32(src.data_ptr(), src.stride(0), idx.data_ptr(),
+                                              dst.data_ptr(), dst.stride(0), rows, src.shape[1],
+                                              _stream()), "sp_gather_rows_f32")
+    _count()

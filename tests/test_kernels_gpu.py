@@ -1,0 +1,309 @@
+"""Per-kernel numerics of libshiftpar.so on a B200 vs plain fp32 torch references.
+
+Tolerances: the kernels read bf16 operands and accumulate in f32, exactly like
+the fp32 reference computed from the same bf16 values, so f32 outputs agree to
+accumulation-order noise (<=1e-4 of the output scale) and bf16 outputs to one
+bf16 ulp (<=1e-2 relative of the output scale).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+ops = pytest.importorskip("paper_2507_11830_b200.ops")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ops.device_check()
+
+
+def rnd(*shape, scale=1.0, seed=0, dtype=torch.bfloat16):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return (torch.randn(*shape, generator=g, device="cuda") * scale).to(dtype)
+
+
+def rel(a, b):
+    return float((a.float() - b.float()).abs().max() / b.float().abs().max().clamp_min(1e-30))
+
+
+GEMM_SHAPES = [(1, 256, 64), (7, 384, 256), (128, 256, 4096), (300, 512, 1024), (1000, 768, 512),
+               (257, 6144, 4096), (2048, 1024, 2048), (64, 96, 128)]
+
+
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_gemm_f32_and_bf16(M, N, K):
+    a, b = rnd(M, K, seed=1), rnd(N, K, seed=2)
+    ref = a.float() @ b.float().t()
+    d32 = torch.empty(M, N, device="cuda")
+    ops.gemm(a, b, d32, ops.EPI_STORE_F32, M=M, N=N, K=K, lda=K, ldb=K, ldd=N)
+    assert rel(d32, ref) < 1e-4
+    d16 = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    ops.gemm(a, b, d16, ops.EPI_STORE_BF16, M=M, N=N, K=K, lda=K, ldb=K, ldd=N)
+    assert rel(d16, ref) < 1e-2
+
+
+def test_gemm_add_f32_residual():
+    M, N, K = 333, 512, 768
+    a, b = rnd(M, K, seed=3), rnd(N, K, seed=4)
+    x = torch.randn(M, N, device="cuda")
+    want = x + a.float() @ b.float().t()
+    ops.gemm(a, b, x, ops.EPI_ADD_F32, M=M, N=N, K=K, lda=K, ldb=K, ldd=N)
+    assert rel(x, want) < 1e-4
+
+
+def test_gemm_swiglu_interleaved():
+    M, f, K = 200, 512, 256
+    a = rnd(M, K, seed=5)
+    gate, up = rnd(f, K, seed=6), rnd(f, K, seed=7)
+    w = torch.empty(2 * f, K, device="cuda", dtype=torch.bfloat16)
+    v = w.view(f // 128, 2, 128, K)
+    v[:, 0] = gate.view(f // 128, 128, K)
+    v[:, 1] = up.view(f // 128, 128, K)
+    g = a.float() @ gate.float().t()
+    u = a.float() @ up.float().t()
+    want = torch.nn.functional.silu(g) * u
+    d = torch.empty(M, f, device="cuda", dtype=torch.bfloat16)
+    ops.gemm(a, w, d, ops.EPI_SWIGLU, M=M, N=2 * f, K=K, lda=K, ldb=K, ldd=f)
+    assert rel(d, want) < 1e-2
+
+
+def test_gemm_gelu():
+    M, N, K = 100, 256, 128
+    a, b = rnd(M, K, seed=8), rnd(N, K, seed=9)
+    want = torch.nn.functional.gelu(a.float() @ b.float().t(), approximate="tanh")
+    d = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    ops.gemm(a, b, d, ops.EPI_GELU, M=M, N=N, K=K, lda=K, ldb=K, ldd=N)
+    assert rel(d, want) < 1e-2
+
+
+def test_gemm_peer_layout_and_chunked_a():
+    P, rows, W, K = 4, 37, 96, 256
+    a, b = rnd(rows, K, seed=10), rnd(P * W, K, seed=11)
+    ref = torch.empty(rows, P * W, device="cuda", dtype=torch.bfloat16)
+    ops.gemm(a, b, ref, ops.EPI_STORE_BF16, M=rows, N=P * W, K=K, lda=K, ldb=K, ldd=P * W)
+    assert rel(ref, a.float() @ b.float().t()) < 1e-2
+    send = torch.empty(P * rows, W, device="cuda", dtype=torch.bfloat16)
+    ops.gemm(a, b, send, ops.EPI_STORE_BF16, M=rows, N=P * W, K=K, lda=K, ldb=K, ldd=W,
+             peer_width=W, peer_stride=rows * W)
+    for s in range(P):
+        assert torch.equal(send[s * rows:(s + 1) * rows], ref[:, s * W:(s + 1) * W])
+    # chunked-K A: back[P][rows][w] acts as A[rows, P*w]
+    w = 128
+    back = rnd(P * rows, w, seed=12)
+    flat = torch.cat([back[s * rows:(s + 1) * rows] for s in range(P)], dim=1)
+    wo = rnd(256, P * w, seed=13)
+    want = flat.float() @ wo.float().t()
+    d = torch.zeros(rows, 256, device="cuda")
+    ops.gemm(back, wo, d, ops.EPI_ADD_F32, M=rows, N=256, K=P * w, lda=w, ldb=P * w, ldd=256,
+             a_kchunk=w, a_chunk_stride=rows * w)
+    assert rel(d, want) < 1e-4
+
+
+def test_gemm_strided_b_window_is_zero_copy_tp_shard():
+    M, N, Kfull, P = 64, 256, 1024, 4
+    a_full, b = rnd(M, Kfull, seed=14), rnd(N, Kfull, seed=15)
+    kl = Kfull // P
+    for r in range(P):
+        a = a_full[:, r * kl:(r + 1) * kl].contiguous()
+        want = a.float() @ b[:, r * kl:(r + 1) * kl].float().t()
+        d = torch.empty(M, N, device="cuda")
+        ops.gemm(a, b[:, r * kl:], d, ops.EPI_STORE_F32, M=M, N=N, K=kl, lda=kl, ldb=Kfull, ldd=N)
+        assert rel(d, want) < 1e-4
+
+
+def test_gemm_row_and_column_splits_bitexact():
+    """tensor_core.py:1-28 property on the GPU: fixed tiles, no split-K."""
+    M, N, K = 700, 1024, 512
+    a, b = rnd(M, K, seed=16), rnd(N, K, seed=17)
+    full = torch.empty(M, N, device="cuda")
+    ops.gemm(a, b, full, ops.EPI_STORE_F32, M=M, N=N, K=K, lda=K, ldb=K, ldd=N)
+    for lo, hi in ((0, 1), (1, 300), (300, 700)):
+        part = torch.empty(hi - lo, N, device="cuda")
+        ops.gemm(a[lo:hi], b, part, ops.EPI_STORE_F32, M=hi - lo, N=N, K=K, lda=K, ldb=K, ldd=N)
+        assert torch.equal(part, full[lo:hi])
+    for lo, hi in ((0, 256), (256, 768), (768, 1024)):
+        part = torch.empty(M, hi - lo, device="cuda")
+        ops.gemm(a, b[lo:hi], part, ops.EPI_STORE_F32, M=M, N=hi - lo, K=K, lda=K, ldb=K,
+                 ldd=hi - lo)
+        assert torch.equal(part, full[:, lo:hi])
+
+
+def test_embed_and_rmsnorm():
+    V, h, rows = 1000, 512, 77
+    table = rnd(V, h, seed=18)
+    ids = torch.randint(0, V, (rows,), device="cuda", dtype=torch.int32)
+    x = torch.empty(rows, h, device="cuda")
+    ops.embed(ids, table, x)
+    assert torch.equal(x, table[ids.long()].float())
+    gain = torch.rand(h, device="cuda") + 0.5
+    add = torch.randn(rows, h, device="cuda")
+    x0 = x.clone()
+    out = torch.empty(rows, h, device="cuda", dtype=torch.bfloat16)
+    ops.add_rmsnorm(x, gain, 1e-5, out, add=add)
+    xs = x0 + add
+    assert torch.allclose(x, xs)
+    want = gain * (xs / torch.sqrt((xs * xs).mean(-1, keepdim=True) + 1e-5))
+    assert rel(out, want) < 1e-2
+    idx = torch.tensor([3, 0, 76], device="cuda", dtype=torch.int32)
+    o2 = torch.empty(3, h, device="cuda", dtype=torch.bfloat16)
+    ops.add_rmsnorm(x, gain, 1e-5, o2, row_idx=idx)
+    assert torch.equal(o2, out[idx.long()])
+
+
+def _rope_ref(x, pos, tab):
+    d = x.shape[-1]
+    c = tab[pos.long(), :, 0][:, None, :]
+    s = tab[pos.long(), :, 1][:, None, :]
+    lo, hi = x[..., :d // 2], x[..., d // 2:]
+    return torch.cat([lo * c - hi * s, hi * c + lo * s], dim=-1)
+
+
+def test_rope_kv_write_paged():
+    from paper_2507_11830_b200.weights import rope_table
+    hq, hk, d, bs, nblk, rows = 4, 2, 64, 16, 10, 40
+    tab = torch.as_tensor(rope_table(256, d, 500000.0, None), device="cuda")
+    qkv = rnd(rows, (hq + 2 * hk) * d, seed=19)
+    pos = torch.arange(5, 5 + rows, device="cuda", dtype=torch.int32)
+    perm = torch.randperm(nblk * bs, device="cuda")[:rows].to(torch.int32)
+    kpool = torch.zeros(nblk, hk, bs, d, device="cuda", dtype=torch.bfloat16)
+    vpool = torch.zeros_like(kpool)
+    q = torch.empty(rows, hq * d, device="cuda", dtype=torch.bfloat16)
+    ops.rope_kv_write(qkv, pos, perm, tab, q, kpool, vpool, rows=rows, q_heads=hq, kv_heads=hk,
+                      head_dim=d, block_size=bs)
+    x = qkv.float().view(rows, hq + 2 * hk, d)
+    q_ref = _rope_ref(x[:, :hq], pos, tab)
+    k_ref = _rope_ref(x[:, hq:hq + hk], pos, tab)
+    assert rel(q.view(rows, hq, d), q_ref) < 1e-2
+    blk, off = (perm // bs).long(), (perm % bs).long()
+    got_k = kpool[blk, :, off]  # [rows, hk, d]
+    got_v = vpool[blk, :, off]
+    assert rel(got_k, k_ref) < 1e-2
+    assert torch.equal(got_v, qkv.view(rows, hq + 2 * hk, d)[:, hq + hk:])
+
+
+def _attn_ref(q, k, v, first_pos):
+    """q [m, H, d], k/v [T, Hkv, d] -> [m, H, d] with causal window semantics."""
+    m, H, d = q.shape
+    T, Hk, _ = k.shape
+    G = H // Hk
+    out = torch.empty(m, H, d, device=q.device)
+    for hh in range(H):
+        s = q[:, hh].float() @ k[:, hh // G].float().t() / d ** 0.5
+        ok = torch.arange(T, device=q.device)[None] <= (first_pos + torch.arange(m, device=q.device))[:, None]
+        s = s.masked_fill(~ok, float("-inf"))
+        out[:, hh] = torch.softmax(s, -1) @ v[:, hh // G].float()
+    return out
+
+
+def _paged(kv_list, hk, d, bs):
+    """Scatter per-item [T, hk, d] into a pool with a shuffled block table."""
+    nblk = sum(-(-t.shape[0] // bs) for t in kv_list) + 3
+    order = torch.randperm(nblk).tolist()
+    pool = torch.zeros(nblk, hk, bs, d, device="cuda", dtype=torch.bfloat16)
+    tables, nxt = [], 0
+    for t in kv_list:
+        nb = -(-t.shape[0] // bs)
+        tab = order[nxt:nxt + nb]
+        nxt += nb
+        for j in range(t.shape[0]):
+            pool[tab[j // bs], :, j % bs] = t[j]
+        tables.append(tab)
+    width = max(len(t) for t in tables)
+    bt = torch.zeros(len(tables), width, dtype=torch.int32, device="cuda")
+    for i, t in enumerate(tables):
+        bt[i, :len(t)] = torch.tensor(t, dtype=torch.int32)
+    return pool, bt
+
+
+@pytest.mark.parametrize("d,hq,hk,bs", [(128, 8, 2, 64), (64, 4, 4, 16), (32, 8, 2, 32),
+                                        (128, 32, 8, 64)])
+def test_attention_prefill_paged_causal(d, hq, hk, bs):
+    torch.manual_seed(0)
+    spans = [37, 130, 1, 64]
+    hist = [0, 20, 70, 5]
+    ks, vs, qs = [], [], []
+    for m, t0 in zip(spans, hist):
+        ks.append(rnd(t0 + m, hk, d, seed=20 + m))
+        vs.append(rnd(t0 + m, hk, d, seed=40 + m))
+        qs.append(rnd(m, hq, d, seed=60 + m))
+    kpool, bt = _paged(ks, hk, d, bs)
+    vpool, bt2 = _paged(vs, hk, d, bs)
+    # same table for k and v: rebuild v with k's table
+    vpool = torch.zeros_like(kpool)
+    for i, t in enumerate(vs):
+        tab = bt[i].tolist()
+        for j in range(t.shape[0]):
+            vpool[tab[j // bs], :, j % bs] = t[j]
+    q = torch.cat(qs).view(-1, hq * d)
+    M = q.shape[0]
+    cu = torch.tensor([0] + list(np.cumsum(spans)), dtype=torch.int32, device="cuda")
+    first = torch.tensor(hist, dtype=torch.int32, device="cuda")
+    kvl = torch.tensor([a + b for a, b in zip(spans, hist)], dtype=torch.int32, device="cuda")
+    tt = ops.attn_tile_tokens(hq, hk)
+    work = [(i, t0) for i, m in enumerate(spans) for t0 in range(0, m, tt)]
+    work_t = torch.tensor(work, dtype=torch.int32, device="cuda").view(-1)
+    out = torch.empty(M, hq * d, device="cuda", dtype=torch.bfloat16)
+    ops.attention(q, kpool, vpool, bt, cu, first, kvl, out, n_items=len(spans), work=work_t,
+                  n_work=len(work), max_q_len=max(spans), max_kv_len=int(kvl.max()), q_heads=hq,
+                  kv_heads=hk, head_dim=d, block_size=bs, ws=None)
+    lo = 0
+    for i, (m, t0) in enumerate(zip(spans, hist)):
+        want = _attn_ref(qs[i], ks[i], vs[i], t0)
+        assert rel(out[lo:lo + m].view(m, hq, d), want) < 2e-2, i
+        lo += m
+
+
+@pytest.mark.parametrize("d,hq,hk,ctx", [(128, 32, 8, 2048), (128, 8, 2, 100), (64, 4, 4, 5000),
+                                         (32, 8, 2, 1)])
+def test_attention_decode_split_kv(d, hq, hk, ctx):
+    n = 5
+    bs = 64
+    ctxs = [ctx + 7 * i for i in range(n)]
+    ks = [rnd(c, hk, d, seed=100 + i) for i, c in enumerate(ctxs)]
+    vs = [rnd(c, hk, d, seed=200 + i) for i, c in enumerate(ctxs)]
+    qs = [rnd(1, hq, d, seed=300 + i) for i in range(n)]
+    kpool, bt = _paged(ks, hk, d, bs)
+    vpool = torch.zeros_like(kpool)
+    for i, t in enumerate(vs):
+        tab = bt[i].tolist()
+        for j in range(t.shape[0]):
+            vpool[tab[j // bs], :, j % bs] = t[j]
+    q = torch.cat(qs).view(n, hq * d)
+    cu = torch.arange(n + 1, dtype=torch.int32, device="cuda")
+    kvl = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+    first = kvl - 1
+    ws = torch.empty(ops.attn_workspace_bytes(n, hq, d, max(ctxs)) // 4, device="cuda")
+    out = torch.empty(n, hq * d, device="cuda", dtype=torch.bfloat16)
+    ops.attention(q, kpool, vpool, bt, cu, first, kvl, out, n_items=n, work=None, n_work=0,
+                  max_q_len=1, max_kv_len=max(ctxs), q_heads=hq, kv_heads=hk, head_dim=d,
+                  block_size=bs, ws=ws)
+    for i in range(n):
+        want = _attn_ref(qs[i], ks[i], vs[i], ctxs[i] - 1)
+        assert rel(out[i].view(1, hq, d), want) < 2e-2, i
+
+
+def test_pack_unpack_roundtrip_and_add_argmax():
+    rows, P, w = 33, 4, 64
+    src = rnd(rows, P * w, seed=400)
+    packed = torch.empty(P * rows, w, device="cuda", dtype=torch.bfloat16)
+    ops.a2a_pack(src, packed, rows, P, w)
+    for s in range(P):
+        assert torch.equal(packed[s * rows:(s + 1) * rows], src[:, s * w:(s + 1) * w])
+    back = torch.empty_like(src)
+    ops.a2a_unpack(packed, back, rows, P, w)
+    assert torch.equal(back, src)
+    a, b = torch.randn(1001, device="cuda"), torch.randn(1001, device="cuda")
+    c = torch.empty_like(a)
+    ops.add_f32(a, b, c)
+    assert torch.equal(c, a + b)
+    lg = torch.randn(6, 50000, device="cuda")
+    lg[2, 7] = lg[2, 9] = 1e4  # tie -> lowest index (model.py:303-307)
+    idx = torch.empty(6, dtype=torch.int32, device="cuda")
+    ops.argmax(lg, idx)
+    want = lg.argmax(-1).to(torch.int32)
+    assert torch.equal(idx, want) and int(idx[2]) == 7
