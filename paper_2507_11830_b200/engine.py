@@ -394,6 +394,7 @@ class Engine:
             views[k] = (off, a.size)
             off += -(-a.size // 4) * 4
         dev[:total].copy_(host[:total], non_blocking=True)
+        self.last_h2d_bytes = total * 4
         ev = torch.cuda.Event()
         ev.record()
         self._pin_events[idx] = ev
@@ -437,12 +438,17 @@ class Engine:
             decode_like = meta.decode_like
             spans = meta.spans
         ws = self._workspace(meta.n, hq, meta.max_kv) if decode_like else None
+        # algorithmic work: causal half of q·Kᵀ + P·V, and K/V bytes streamed
+        hist = [w - m for m, w in zip(spans, meta.windows)]
+        causal = sum(m * t0 + m * (m + 1) // 2 for m, t0 in zip(spans, hist))
+        kv_bytes = sum(meta.windows) * hk * d * 2 * 2
         ops.attention(q, self.pool.layer_k(r, layer), self.pool.layer_v(r, layer), meta.bt, cu,
                       first, meta.kvlen, out, n_items=meta.n,
                       work=None if decode_like else meta.work_pairs,
                       n_work=0 if decode_like else meta.n_work, max_q_len=max(spans),
                       max_kv_len=meta.max_kv, q_heads=hq, kv_heads=hk, head_dim=d,
-                      block_size=self.pool.block_size, ws=ws)
+                      block_size=self.pool.block_size, ws=ws, work_flops=4 * d * hq * causal,
+                      work_bytes=kv_bytes)
         # reference meter: per item per owned head, q·Kᵀ and P·V over the full window
         for m, w in zip(spans, meta.windows):
             meter.add_matmul(hq * m, d, w)

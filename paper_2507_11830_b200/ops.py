@@ -24,10 +24,32 @@ EPI_GELU = 4
 
 launch_count = 0
 
+# Optional live per-kernel timing (bench.py roofline): when set to a dict, the
+# wrapped launches record CUDA events on the launching stream plus their
+# algorithmic work: PROFILE[kind] -> list of (start, end, flops, bytes).
+PROFILE: Optional[dict] = None
+
 
 def _count(n: int = 1) -> None:
     global launch_count
     launch_count += n
+
+
+class _Timed:
+    def __init__(self, kind: str, flops: int = 0, nbytes: int = 0):
+        self.kind, self.flops, self.nbytes = kind, flops, nbytes
+
+    def __enter__(self):
+        if PROFILE is not None:
+            self.ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            self.ev[0].record()
+        return self
+
+    def __exit__(self, *exc):
+        if PROFILE is not None and exc[0] is None:
+            self.ev[1].record()
+            PROFILE.setdefault(self.kind, []).append((self.ev[0], self.ev[1], self.flops, self.nbytes))
+        return False
 
 
 def _stream() -> int:
@@ -68,8 +90,11 @@ def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, epilogue: int, *, M:
     if M == 0:
         return
     lib = _lib.load()
-    rc = lib.sp_gemm_bf16(a.data_ptr(), lda, a_kchunk, a_chunk_stride, b.data_ptr(), ldb,
-                          d.data_ptr(), ldd, M, N, K, epilogue, peer_width, peer_stride, _stream())
+    nbytes = (M * K + N * K) * 2 + M * (N // 2 if epilogue == EPI_SWIGLU else N) * d.element_size()
+    with _Timed("gemm", 2 * M * N * K, nbytes):
+        rc = lib.sp_gemm_bf16(a.data_ptr(), lda, a_kchunk, a_chunk_stride, b.data_ptr(), ldb,
+                              d.data_ptr(), ldd, M, N, K, epilogue, peer_width, peer_stride,
+                              _stream())
     _lib.check(rc, "sp_gemm_bf16")
     _count()
 
@@ -134,18 +159,20 @@ def attention(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
               kv_len: torch.Tensor, out: torch.Tensor, *, n_items: int,
               work: Optional[torch.Tensor], n_work: int, max_q_len: int, max_kv_len: int,
               q_heads: int, kv_heads: int, head_dim: int, block_size: int,
-              ws: Optional[torch.Tensor]) -> None:
+              ws: Optional[torch.Tensor], work_flops: int = 0, work_bytes: int = 0) -> None:
     _need(q, torch.bfloat16, "attention q")
     _need(out, torch.bfloat16, "attention out")
     if n_items == 0:
         return
     ws_bytes = 0 if ws is None else ws.numel() * ws.element_size()
-    rc = _lib.load().sp_attention(q.data_ptr(), q.stride(0), k_pool.data_ptr(), v_pool.data_ptr(),
-                                  block_tables.data_ptr(), block_tables.stride(0), cu_q.data_ptr(),
-                                  first_pos.data_ptr(), kv_len.data_ptr(), n_items, _ptr(work),
-                                  n_work, max_q_len, max_kv_len, out.data_ptr(), out.stride(0),
-                                  q_heads, kv_heads, head_dim, block_size, _ptr(ws), ws_bytes,
-                                  _stream())
+    kind = "attn_prefill" if n_work > 0 else "attn_decode"
+    with _Timed(kind, work_flops, work_bytes):
+        rc = _lib.load().sp_attention(q.data_ptr(), q.stride(0), k_pool.data_ptr(), v_pool.data_ptr(),
+                                      block_tables.data_ptr(), block_tables.stride(0),
+                                      cu_q.data_ptr(), first_pos.data_ptr(), kv_len.data_ptr(),
+                                      n_items, _ptr(work), n_work, max_q_len, max_kv_len,
+                                      out.data_ptr(), out.stride(0), q_heads, kv_heads, head_dim,
+                                      block_size, _ptr(ws), ws_bytes, _stream())
     _lib.check(rc, "sp_attention")
     _count(1 if n_work > 0 else 2)
 
