@@ -281,7 +281,7 @@ def run_ours(args):
                 "traffic": None}
     attn = None
     if a:
-        attn = {"kernel": "sp_attention prefill (paged, GQA-packed, mma.sync)",
+        attn = {"kernel": "sp_attention prefill (tcgen05/TMEM, paged, GQA-packed)",
                 "achieved_tflops": round(a[1] / (a[0] / 1e3) / 1e12, 1),
                 "share_of_step": round(a[0] / elapsed_ms, 4), "launches": a[3],
                 "causal_flops_per_step": a[1] // args.steps}

@@ -112,16 +112,20 @@ sp_status sp_rope_kv_write(const void* qkv, int64_t ldqkv, const int32_t* pos,
  * work: int32 pairs (item, first q row of a tile) — host-built schedule;
  * pass n_work = 0 to let the call build the decode schedule (1 row/item).
  * ws: f32 workspace of sp_attn_workspace_bytes() bytes (split-KV partials).
+ * q_rows: rows of the q buffer; pool_blocks: blocks of the (per-layer) pool.
  */
-sp_status sp_attention(const void* q, int64_t ldq, const void* k_pool, const void* v_pool,
-                       const int32_t* block_tables, int64_t bt_stride, const int32_t* cu_q,
+sp_status sp_attention(const void* q, int64_t ldq, int64_t q_rows, const void* k_pool,
+                       const void* v_pool, int64_t pool_blocks, const int32_t* block_tables,
+                       int64_t bt_stride, const int32_t* cu_q,
                        const int32_t* first_pos, const int32_t* kv_len, int n_items,
                        const int32_t* work, int n_work, int max_q_len, int max_kv_len,
                        void* out, int64_t ldo, int q_heads, int kv_heads, int head_dim,
                        int block_size, void* ws, int64_t ws_bytes, void* stream);
 int64_t sp_attn_workspace_bytes(int n_items, int q_heads, int head_dim, int max_kv_len);
-/* Rows per prefill work tile for a (q_heads, kv_heads) pair (host schedule). */
-int sp_attn_tile_tokens(int q_heads, int kv_heads);
+/* Tokens per prefill work tile (host schedule).  head_dim 128 with pages of a
+ * multiple of 64 keys selects the tcgen05/TMEM kernel (2 x 128 packed rows
+ * per CTA); other shapes use the mma.sync kernel (64 packed rows). */
+int sp_attn_tile_tokens(int q_heads, int kv_heads, int head_dim, int block_size);
 
 /* ------------------------------------------- all-to-all pack / unpack
  * The reference re-shards with np.ascontiguousarray(tensor[:, lo:hi, :])

@@ -31,11 +31,11 @@ SIGNATURES = {
     "sp_add_rmsnorm": (_c_int, [_vp, _i64, _vp, _vp, _f32, _vp, _vp, _i64, _c_int, _c_int, _vp]),
     "sp_rope_kv_write": (_c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _c_int, _c_int,
                                   _c_int, _c_int, _c_int, _vp]),
-    "sp_attention": (_c_int, [_vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _c_int, _vp, _c_int,
-                              _c_int, _c_int, _vp, _i64, _c_int, _c_int, _c_int, _c_int, _vp, _i64,
-                              _vp]),
+    "sp_attention": (_c_int, [_vp, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _c_int,
+                              _vp, _c_int, _c_int, _c_int, _vp, _i64, _c_int, _c_int, _c_int,
+                              _c_int, _vp, _i64, _vp]),
     "sp_attn_workspace_bytes": (_i64, [_c_int, _c_int, _c_int, _c_int]),
-    "sp_attn_tile_tokens": (_c_int, [_c_int, _c_int]),
+    "sp_attn_tile_tokens": (_c_int, [_c_int, _c_int, _c_int, _c_int]),
     "sp_a2a_pack": (_c_int, [_vp, _i64, _vp, _c_int, _c_int, _c_int, _vp]),
     "sp_a2a_unpack": (_c_int, [_vp, _vp, _i64, _c_int, _c_int, _c_int, _vp]),
     "sp_add_f32": (_c_int, [_vp, _vp, _vp, _i64, _vp]),

@@ -454,11 +454,27 @@ static int decode_splits(int n_items, int kv_heads, int max_kv_len) {
 }  // namespace attn
 }  // namespace sp
 
+namespace sp {
+int launch_prefill_tc(const void* q, int64_t ldq, int64_t q_rows_total, const void* k_pool,
+                      const void* v_pool, int64_t pool_rows, const int32_t* block_tables,
+                      int64_t bt_stride, const int32_t* cu_q, const int32_t* first_pos,
+                      const int32_t* kv_len, const int32_t* work, int n_work, void* out,
+                      int64_t ldo, int q_heads, int kv_heads, int block_size, cudaStream_t st);
+}
+
 using namespace sp;
 
-extern "C" int sp_attn_tile_tokens(int q_heads, int kv_heads) {
+// tcgen05 prefill kernel: head_dim 128, pages of 64*k keys, GQA group dividing 128
+static bool use_tc_prefill(int q_heads, int kv_heads, int head_dim, int block_size) {
+  if (kv_heads <= 0 || q_heads % kv_heads) return false;
+  const int g = q_heads / kv_heads;
+  return head_dim == 128 && block_size % 64 == 0 && g <= 16 && 128 % g == 0;
+}
+
+extern "C" int sp_attn_tile_tokens(int q_heads, int kv_heads, int head_dim, int block_size) {
   if (kv_heads <= 0 || q_heads % kv_heads) return 0;
   const int g = q_heads / kv_heads;
+  if (use_tc_prefill(q_heads, kv_heads, head_dim, block_size)) return 256 / g;
   return g > attn::PF_ROWS ? 0 : attn::PF_ROWS / g;
 }
 
@@ -468,7 +484,8 @@ extern "C" int64_t sp_attn_workspace_bytes(int n_items, int q_heads, int head_di
   return (int64_t)n_items * q_heads * splits * (head_dim + 1) * 4;
 }
 
-extern "C" sp_status sp_attention(const void* q, int64_t ldq, const void* k_pool, const void* v_pool,
+extern "C" sp_status sp_attention(const void* q, int64_t ldq, int64_t q_rows, const void* k_pool,
+                                  const void* v_pool, int64_t pool_blocks,
                                   const int32_t* block_tables, int64_t bt_stride, const int32_t* cu_q,
                                   const int32_t* first_pos, const int32_t* kv_len, int n_items,
                                   const int32_t* work, int n_work, int max_q_len, int max_kv_len,
@@ -516,6 +533,14 @@ extern "C" sp_status sp_attention(const void* q, int64_t ldq, const void* k_pool
     }
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (n_work > 0 && use_tc_prefill(q_heads, kv_heads, head_dim, block_size)) {
+    if (ldq % 8 || ldo % 8 || q_rows <= 0 || pool_blocks <= 0)
+      return fail(kInvalid, "attention: tcgen05 prefill needs 16-byte rows and sizes");
+    return launch_prefill_tc(q, ldq, q_rows, k_pool, v_pool,
+                             pool_blocks * (int64_t)kv_heads * block_size, block_tables, bt_stride,
+                             cu_q, first_pos, kv_len, work, n_work, out, ldo, q_heads, kv_heads,
+                             block_size, st);
+  }
   switch (head_dim) {
     case 32: return attn::launch<32>(p, n_items, n_work, st);
     case 64: return attn::launch<64>(p, n_items, n_work, st);

@@ -1,0 +1,393 @@
+// tcgen05 / TMEM / TMA paged causal prefill attention for sm_100a (head_dim 128).
+//
+// Same contract as the mma.sync prefill kernel in attention.cu (reference
+// tensor_core.attend_cached, tensor_core.py:135-176), selected by sp_attention
+// when head_dim == 128 and the pool's block_size is a multiple of 64.
+//
+// One CTA = one kv head x two 128-row query tiles of GQA-packed rows
+// (row = token * G + head-in-group, so one K/V tile feeds all G heads):
+//   warps 0-3  softmax warpgroup for Q tile 0 (one TMEM lane = one row per thread)
+//   warps 4-7  softmax warpgroup for Q tile 1
+//   warp 8     TMA producer: Q tiles once (3-D map over [tokens][G][d]), then
+//              128-key K/V tiles page by page from the paged pool (2-stage ring)
+//   warp 9     TMEM allocator + single-thread MMA issuer
+// TMEM (512 cols): S0 | S1 (128 f32 cols each; P_i is written back as bf16 over
+// the first 64 columns of S_i and consumed as the TMEM A-operand of P·V) |
+// O0 | O1 (128 f32 cols each).  MMA issue order per key tile j:
+//   PV0_j, QK0_{j+1}, PV1_j, QK1_{j+1}  — softmax i works on S_i(j+1) while the
+// tensor core runs the other tile's PV/QK.  O is rescaled lazily by the softmax
+// warps (only when a row max grows by > 2^8), safe because the commit that
+// signals S_i(j+1) also covers PV_i(j).
+#include <cudaTypedefs.h>
+
+#include "../../include/shiftpar.h"
+#include "common.cuh"
+
+namespace sp {
+namespace attn_tc {
+
+constexpr int HD = 128;
+constexpr int QROWS = 128;       // rows per Q tile
+constexpr int KT = 128;          // keys per tile
+constexpr int NUM_THREADS = 320;
+constexpr int Q_TILE_BYTES = QROWS * HD * 2;      // 32 KiB (two 64-wide d chunks)
+constexpr int KV_TILE_BYTES = KT * HD * 2;        // 32 KiB
+constexpr int SMEM_Q = 2 * Q_TILE_BYTES;
+constexpr int SMEM_KV = 2 * 2 * KV_TILE_BYTES;    // 2 stages x (K, V)
+constexpr int SMEM_BYTES = SMEM_Q + SMEM_KV + 1024 + 256;
+constexpr float kRescaleThreshold = 8.0f;         // log2 units
+
+struct Params {
+  const int32_t* block_tables;
+  int64_t bt_stride;
+  const int32_t* cu_q;
+  const int32_t* first_pos;
+  const int32_t* kv_len;
+  const int2* work;
+  __nv_bfloat16* out;
+  int64_t ldo;
+  int kv_heads, group, block_size;
+  float scale_log2;
+};
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+
+__device__ __forceinline__ void tmem_st_wait() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// D[tmem] (+)= A[tmem] * B[smem]   (A = P, bf16 packed two per 32-bit column)
+__device__ __forceinline__ void umma_ts_bf16(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// MN-major (N contiguous) 128-byte-swizzle descriptor: 64-element rows of
+// 128 B along N, 8-row atoms SBO = 1024 B apart along K, next 64-wide N
+// chunk LBO bytes away.
+__device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t smem_addr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    prefill_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                      const __grid_constant__ CUtensorMap tmV, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;                 // [tile][dchunk][128 rows][128 B]
+  uint8_t* sKV = smem + SMEM_Q;       // [stage][K | V][dchunk][128 keys][128 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_Q + SMEM_KV);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;   // [2]
+  uint64_t* v_full = bars + 3;   // [2]
+  uint64_t* kv_empty = bars + 5; // [2]
+  uint64_t* s_full = bars + 7;   // [2] per Q tile
+  uint64_t* p_full = bars + 9;   // [2] per Q tile
+  uint64_t* o_full = bars + 11;  // [2] per Q tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int2 wk = p.work[blockIdx.x];
+  const int item = wk.x, tok0 = wk.y;
+  const int kvh = blockIdx.y;
+  const int G = p.group;
+  const int q_row0 = p.cu_q[item];
+  const int q_len = p.cu_q[item + 1] - q_row0;
+  const int fpos = p.first_pos[item];
+  const int kv_len = p.kv_len[item];
+  const int toks_per_tile = QROWS / G;
+  const int tok_last = min(tok0 + 2 * toks_per_tile, q_len) - 1;
+  const int kv_end = min(kv_len, fpos + tok_last + 1);
+  const int n_kt = (kv_end + KT - 1) / KT;
+  const int n_pages = (kv_len + p.block_size - 1) / p.block_size;
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(k_full + s, 1);
+      mbar_init(v_full + s, 1);
+      mbar_init(kv_empty + s, 1);
+      mbar_init(s_full + s, 1);
+      mbar_init(p_full + s, 128);
+      mbar_init(o_full + s, 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, SMEM_Q);
+      for (int t = 0; t < 2; ++t)
+        for (int c = 0; c < 2; ++c)
+          tma_load_3d(sQ + t * Q_TILE_BYTES + c * (Q_TILE_BYTES / 2), &tmQ, q_full, c * 64,
+                      kvh * G, q_row0 + tok0 + t * toks_per_tile);
+      const int32_t* bt = p.block_tables + (int64_t)item * p.bt_stride;
+      for (int j = 0; j < n_kt; ++j) {
+        const int s = j & 1;
+        mbar_wait(kv_empty + s, ((j >> 1) & 1) ^ 1);
+        uint8_t* sK = sKV + s * 2 * KV_TILE_BYTES;
+        uint8_t* sV = sK + KV_TILE_BYTES;
+        int rows[2];
+        for (int h = 0; h < 2; ++h) {
+          const int key0 = j * KT + h * 64;
+          const int pg_i = key0 / p.block_size;
+          const int page = pg_i < n_pages ? bt[pg_i] : 0;
+          rows[h] = (page * p.kv_heads + kvh) * p.block_size + key0 % p.block_size;
+        }
+        mbar_arrive_expect_tx(k_full + s, KV_TILE_BYTES);
+        for (int c = 0; c < 2; ++c)
+          for (int h = 0; h < 2; ++h)
+            tma_load_2d(sK + c * (KV_TILE_BYTES / 2) + h * 8192, &tmK, k_full + s, c * 64, rows[h]);
+        mbar_arrive_expect_tx(v_full + s, KV_TILE_BYTES);
+        for (int c = 0; c < 2; ++c)
+          for (int h = 0; h < 2; ++h)
+            tma_load_2d(sV + c * (KV_TILE_BYTES / 2) + h * 8192, &tmV, v_full + s, c * 64, rows[h]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 9) {
+    // ---------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = idesc_bf16_f32(128, KT);
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(128, HD) | (1u << 16);  // B (V) MN-major
+      const uint32_t sq = smem_u32(sQ);
+      mbar_wait(q_full, 0);
+      auto issue_qk = [&](int t, int j) {
+        const int s = j & 1;
+        const uint32_t sk = smem_u32(sKV + s * 2 * KV_TILE_BYTES);
+        const uint32_t qa = sq + t * Q_TILE_BYTES;
+        const uint32_t d_tmem = tmem + t * 128;
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t off = (k >> 2) * (Q_TILE_BYTES / 2) + (k & 3) * 32;
+          const uint32_t koff = (k >> 2) * (KV_TILE_BYTES / 2) + (k & 3) * 32;
+          umma_bf16(d_tmem, sdesc_sw128(qa + off), sdesc_sw128(sk + koff), idesc_qk, k > 0 ? 1u : 0u);
+        }
+        umma_commit(s_full + t);
+      };
+      mbar_wait(k_full + 0, 0);
+      tc_fence_after();
+      issue_qk(0, 0);
+      issue_qk(1, 0);
+      for (int j = 0; j < n_kt; ++j) {
+        const int s = j & 1;
+        const uint32_t par = (j >> 1) & 1;
+        mbar_wait(v_full + s, par);
+        const uint32_t sv = smem_u32(sKV + s * 2 * KV_TILE_BYTES + KV_TILE_BYTES);
+        const bool more = j + 1 < n_kt;
+        if (more) mbar_wait(k_full + (s ^ 1), ((j + 1) >> 1) & 1);
+        for (int t = 0; t < 2; ++t) {
+          mbar_wait(p_full + t, j & 1);
+          tc_fence_after();
+          const uint32_t p_tmem = tmem + t * 128;
+          const uint32_t o_tmem = tmem + 256 + t * 128;
+#pragma unroll
+          for (int k = 0; k < KT / 16; ++k) {
+            umma_ts_bf16(o_tmem, p_tmem + k * 8, sdesc_sw128_mn(sv + k * 2048, KV_TILE_BYTES / 2),
+                         idesc_pv, (j | k) != 0 ? 1u : 0u);
+          }
+          if (more)
+            issue_qk(t, j + 1);
+          else
+            umma_commit(o_full + t);
+        }
+        umma_commit(kv_empty + s);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ----------------------------------------------------- softmax warpgroups
+    const int t = warp >> 2;            // Q tile
+    const int quarter = warp & 3;       // TMEM lane quarter
+    const int row = quarter * 32 + lane;
+    const int prow = t * QROWS + row;   // packed row in the CTA
+    const int tok = tok0 + prow / G;
+    const int head = kvh * G + prow % G;
+    const int limit = fpos + min(tok, q_len - 1);
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t s_tmem = tmem + lane_base + t * 128;
+    const uint32_t o_tmem = tmem + lane_base + 256 + t * 128;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < n_kt; ++j) {
+      mbar_wait(s_full + t, j & 1);
+      tc_fence_after();
+      float s[KT];
+#pragma unroll
+      for (int c = 0; c < KT / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(s_tmem + c * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(r[e]) * p.scale_log2;
+      }
+      const int kbase = j * KT;
+      if (kbase + KT - 1 > limit) {
+#pragma unroll
+        for (int e = 0; e < KT; ++e)
+          if (kbase + e > limit) s[e] = -INFINITY;
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < KT; ++e) mx = fmaxf(mx, s[e]);
+      const float m_new = fmaxf(m_run, mx);
+      const bool need = m_new > m_run + kRescaleThreshold;
+      float corr = 1.f;
+      if (need) {
+        corr = exp2f(m_run - m_new);
+        m_run = m_new;
+      }
+      l_run *= corr;
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+#pragma unroll 1
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(o_tmem + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * corr);
+          tmem_st32(o_tmem + c * 32, r);
+        }
+        tmem_st_wait();
+      }
+      float sum = 0.f;
+#pragma unroll
+      for (int c = 0; c < KT / 64; ++c) {
+        uint32_t pk[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const float a = exp2f(s[c * 64 + 2 * e] - m_run);
+          const float b = exp2f(s[c * 64 + 2 * e + 1] - m_run);
+          sum += a + b;
+          pk[e] = pack_bf16x2(a, b);
+        }
+        tmem_st32(s_tmem + c * 32, pk);
+      }
+      l_run += sum;
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(p_full + t);
+    }
+    // ------------------------------------------------------------- epilogue
+    mbar_wait(o_full + t, 0);
+    tc_fence_after();
+    const float inv = 1.f / l_run;
+    const bool store = tok < q_len;
+    __nv_bfloat16* dst = p.out + (int64_t)(q_row0 + tok) * p.ldo + (int64_t)head * HD;
+#pragma unroll 1
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld32(o_tmem + c * 32, r);
+      tmem_ld_wait();
+      if (store) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u;
+          u.x = pack_bf16x2(__uint_as_float(r[8 * q + 0]) * inv, __uint_as_float(r[8 * q + 1]) * inv);
+          u.y = pack_bf16x2(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv);
+          u.z = pack_bf16x2(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv);
+          u.w = pack_bf16x2(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv);
+          d4[q] = u;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace attn_tc
+
+// host launcher, called from sp_attention (attention.cu)
+int launch_prefill_tc(const void* q, int64_t ldq, int64_t q_rows_total, const void* k_pool,
+                      const void* v_pool, int64_t pool_rows, const int32_t* block_tables,
+                      int64_t bt_stride, const int32_t* cu_q, const int32_t* first_pos,
+                      const int32_t* kv_len, const int32_t* work, int n_work, void* out,
+                      int64_t ldo, int q_heads, int kv_heads, int block_size, cudaStream_t st);
+
+// tensor maps (shared cache with the GEMM)
+int tma_map_bf16(CUtensorMap* out, const void* ptr, int rank, const uint64_t* dims,
+                 const uint64_t* strides, const uint32_t* box);
+
+int launch_prefill_tc(const void* q, int64_t ldq, int64_t q_rows_total, const void* k_pool,
+                      const void* v_pool, int64_t pool_rows, const int32_t* block_tables,
+                      int64_t bt_stride, const int32_t* cu_q, const int32_t* first_pos,
+                      const int32_t* kv_len, const int32_t* work, int n_work, void* out,
+                      int64_t ldo, int q_heads, int kv_heads, int block_size, cudaStream_t st) {
+  using namespace attn_tc;
+  const int G = q_heads / kv_heads;
+  CUtensorMap tq, tk, tv;
+  {
+    // Q viewed as [tokens][q_heads][d]; the box {64, G, 128/G} at head
+    // coordinate kvh*G picks the G heads of one kv group = 128 packed rows.
+    uint64_t dims[3] = {(uint64_t)HD, (uint64_t)q_heads, (uint64_t)q_rows_total};
+    uint64_t strides[2] = {(uint64_t)HD * 2, (uint64_t)ldq * 2};
+    uint32_t box[3] = {64, (uint32_t)G, (uint32_t)(QROWS / G)};
+    if (int rc = tma_map_bf16(&tq, q, 3, dims, strides, box)) return rc;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)HD, (uint64_t)pool_rows};
+    uint64_t strides[1] = {(uint64_t)HD * 2};
+    uint32_t box[2] = {64, 64};
+    if (int rc = tma_map_bf16(&tk, k_pool, 2, dims, strides, box)) return rc;
+    if (int rc = tma_map_bf16(&tv, v_pool, 2, dims, strides, box)) return rc;
+  }
+  Params p;
+  p.block_tables = block_tables;
+  p.bt_stride = bt_stride;
+  p.cu_q = cu_q;
+  p.first_pos = first_pos;
+  p.kv_len = kv_len;
+  p.work = reinterpret_cast<const int2*>(work);
+  p.out = static_cast<__nv_bfloat16*>(out);
+  p.ldo = ldo;
+  p.kv_heads = kv_heads;
+  p.group = G;
+  p.block_size = block_size;
+  p.scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr = true;
+  }
+  prefill_tc_kernel<<<dim3(n_work, kv_heads), NUM_THREADS, SMEM_BYTES, st>>>(tq, tk, tv, p);
+  return check_launch("attn_prefill_tc_kernel");
+}
+
+}  // namespace sp

@@ -296,7 +296,7 @@ static int encoder() {
 }
 
 // bf16 tiled map with 128-byte swizzle; dims/strides innermost first
-static int get_map(CUtensorMap* out, const void* ptr, int rank, const uint64_t* dims,
+int get_map(CUtensorMap* out, const void* ptr, int rank, const uint64_t* dims,
                    const uint64_t* strides, const uint32_t* box) {
   std::array<uint64_t, 12> key{};
   key[0] = reinterpret_cast<uint64_t>(ptr);
@@ -335,6 +335,12 @@ static int sm_count() {
 }
 
 }  // namespace gemm
+
+int tma_map_bf16(CUtensorMap* out, const void* ptr, int rank, const uint64_t* dims,
+                 const uint64_t* strides, const uint32_t* box) {
+  return gemm::get_map(out, ptr, rank, dims, strides, box);
+}
+
 }  // namespace sp
 
 using namespace sp;

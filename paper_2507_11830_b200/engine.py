@@ -362,7 +362,7 @@ class Engine:
         if decode_like:
             work = np.zeros((0, 2), dtype=np.int32)
         else:
-            tt = ops.attn_tile_tokens(cfg.n_heads // P, cfg.kv_heads // P)
+            tt = ops.attn_tile_tokens(cfg.n_heads // P, cfg.kv_heads // P, cfg.head_dim, bs)
             wl = [(i, t0, hist[i] + t0) for i in range(n) for t0 in range(0, spans[i], tt)]
             wl.sort(key=lambda w: -w[2])  # heaviest causal tiles first
             work = np.asarray([(i, t0) for i, t0, _ in wl], dtype=np.int32).reshape(-1, 2)

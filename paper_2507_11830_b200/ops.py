@@ -146,8 +146,8 @@ def rope_kv_write(qkv: torch.Tensor, pos: torch.Tensor, slot: torch.Tensor,
     _count()
 
 
-def attn_tile_tokens(q_heads: int, kv_heads: int) -> int:
-    return _lib.load().sp_attn_tile_tokens(q_heads, kv_heads)
+def attn_tile_tokens(q_heads: int, kv_heads: int, head_dim: int, block_size: int) -> int:
+    return _lib.load().sp_attn_tile_tokens(q_heads, kv_heads, head_dim, block_size)
 
 
 def attn_workspace_bytes(n_items: int, q_heads: int, head_dim: int, max_kv: int) -> int:
@@ -167,7 +167,8 @@ def attention(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
     ws_bytes = 0 if ws is None else ws.numel() * ws.element_size()
     kind = "attn_prefill" if n_work > 0 else "attn_decode"
     with _Timed(kind, work_flops, work_bytes):
-        rc = _lib.load().sp_attention(q.data_ptr(), q.stride(0), k_pool.data_ptr(), v_pool.data_ptr(),
+        rc = _lib.load().sp_attention(q.data_ptr(), q.stride(0), q.shape[0], k_pool.data_ptr(),
+                                      v_pool.data_ptr(), k_pool.shape[0],
                                       block_tables.data_ptr(), block_tables.stride(0),
                                       cu_q.data_ptr(), first_pos.data_ptr(), kv_len.data_ptr(),
                                       n_items, _ptr(work), n_work, max_q_len, max_kv_len,

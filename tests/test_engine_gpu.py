@@ -324,3 +324,31 @@ def test_compat_mode_against_reference_golden(golden):
                          mode=mode)
         err = rel_err(np.stack(to_np(lg)), arrs[f"c1_{mode.value}2_prefill_logits"])
         assert err <= LOGIT_TOL, (mode, err)
+
+
+@pytest.fixture(scope="module")
+def d128():
+    """head_dim 128 (8B-style heads): exercises the tcgen05/TMEM prefill attention."""
+    cfg = llama_tiny_config(n_layers=2, n_heads=8, n_kv_heads=2, head_dim=128, ffn_dim=1024,
+                            vocab_size=512, max_seq=1024)
+    return init_weights_llama(cfg, seed=2)
+
+
+@pytest.mark.parametrize("mode", [ParallelMode.TP, ParallelMode.SP])
+def test_head_dim_128_tcgen05_attention_matches_oracle(d128, mode):
+    rng = np.random.default_rng(5)
+    prompts = [[int(t) for t in rng.integers(0, 512, size=n)] for n in (300, 17, 129)]
+    eng = make(d128, 2)
+    seqs = [eng.new_sequence(i, capacity=400) for i in range(3)]
+    lg, _ = eng.step(Batch(BatchKind.PREFILL, [BatchItem(s, p) for s, p in zip(seqs, prompts)]),
+                     mode=mode, span_logits=True)
+    for p, got in zip(prompts, lg):
+        want, _ = oracle.forward_reference(d128, p)
+        assert rel_err(got.cpu().numpy(), want) <= LOGIT_TOL
+    # chunked continuation: a second prefill chunk attends over cached history
+    more = [[int(t) for t in rng.integers(0, 512, size=n)] for n in (70, 5, 200)]
+    lg, _ = eng.step(Batch(BatchKind.PREFILL, [BatchItem(s, p) for s, p in zip(seqs, more)]),
+                     mode=mode, span_logits=True)
+    for p, q, got in zip(prompts, more, lg):
+        want, _ = oracle.forward_reference(d128, p + q)
+        assert rel_err(got.cpu().numpy(), want[len(p):]) <= LOGIT_TOL

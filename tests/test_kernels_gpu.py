@@ -244,7 +244,7 @@ def test_attention_prefill_paged_causal(d, hq, hk, bs):
     cu = torch.tensor([0] + list(np.cumsum(spans)), dtype=torch.int32, device="cuda")
     first = torch.tensor(hist, dtype=torch.int32, device="cuda")
     kvl = torch.tensor([a + b for a, b in zip(spans, hist)], dtype=torch.int32, device="cuda")
-    tt = ops.attn_tile_tokens(hq, hk)
+    tt = ops.attn_tile_tokens(hq, hk, d, bs)
     work = [(i, t0) for i, m in enumerate(spans) for t0 in range(0, m, tt)]
     work_t = torch.tensor(work, dtype=torch.int32, device="cuda").view(-1)
     out = torch.empty(M, hq * d, device="cuda", dtype=torch.bfloat16)

@@ -86,7 +86,7 @@ def attn_cases():
         cu = torch.tensor([0, T], dtype=torch.int32, device="cuda")
         first = torch.zeros(1, dtype=torch.int32, device="cuda")
         kvl = torch.tensor([T], dtype=torch.int32, device="cuda")
-        tt = ops.attn_tile_tokens(hq, hk)
+        tt = ops.attn_tile_tokens(hq, hk, d, bs)
         wl = sorted([(0, t0) for t0 in range(0, T, tt)], key=lambda w: -w[1])
         work = torch.tensor(wl, dtype=torch.int32, device="cuda").view(-1)
         o = torch.empty_like(q)
