@@ -1,0 +1,224 @@
+"""CPU-only tests of the product's host side: the C-ABI library loads and
+exports every symbol include/shiftpar.h declares, and the integer/host logic
+(paged allocator, shard bounds, policy, weight layouts, FLOP mirror, KV cache
+bookkeeping) matches the oracle / reference semantics bit-exactly."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle.kvcache import PagedAllocator
+from oracle.model import init_weights_llama, llama_tiny_config
+from oracle.prims import rope_tables, sinusoidal_positions
+
+from helpers import host_dict, product_config
+
+from paper_2507_11830_b200 import (Batch, BatchItem, BatchKind, ConfigError, ContractViolation,
+                                   ParallelMode, PassShape, ShiftPolicy, SwiftKvConfig, choose_mode,
+                                   default_token_threshold, flop_count, partition_heads,
+                                   shard_bounds, shard_rows)
+from paper_2507_11830_b200 import _lib
+from paper_2507_11830_b200.config import llama31_8b, llama33_70b, tiny_llama
+from paper_2507_11830_b200.kv_cache import BlockAllocator, KvCache, KvPool
+from paper_2507_11830_b200.weights import ModelWeights, rope_table, sinusoidal_table
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "shiftpar.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sp_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    import ctypes
+    if not os.path.exists(_lib.LIB_PATH):
+        from paper_2507_11830_b200 import build
+        build.build()
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    syms = header_symbols()
+    assert len(syms) >= 14
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert sorted(_lib.SIGNATURES) == syms
+    loaded = _lib.load()
+    assert loaded.sp_abi_version() == 1
+
+
+def test_library_missing_fails_loudly(monkeypatch, tmp_path):
+    from paper_2507_11830_b200.errors import LibraryMissing
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "nope.so"))
+    with pytest.raises(LibraryMissing):
+        _lib.load()
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2507_11830_b200")
+    for f in os.listdir(pkg):
+        if f.endswith(".py"):
+            src = open(os.path.join(pkg, f)).read()
+            assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), f
+
+
+def test_allocator_matches_oracle_bitexact():
+    rng = np.random.default_rng(0)
+    a, b = BlockAllocator(64, 16), PagedAllocator(64, 16)
+    lens = {}
+    for step in range(300):
+        key = int(rng.integers(0, 8))
+        if rng.random() < 0.15 and key in lens:
+            a.release(key)
+            b.release(key)
+            lens.pop(key)
+            continue
+        n = lens.get(key, 0) + int(rng.integers(1, 40))
+        if a.blocks_needed(key, n) > a.free_blocks:
+            assert b.blocks_needed(key, n) > b.free_blocks
+            continue
+        a.reserve(key, n)
+        b.reserve(key, n)
+        start = lens.get(key, 0)
+        lens[key] = n
+        np.testing.assert_array_equal(a.slots(key, start, n - start),
+                                      b.slots(key, np.arange(start, n)))
+        assert a.tables[key] == b.tables[key]
+    assert a.free_blocks == b.free_blocks
+
+
+def test_shard_bounds_and_partition(golden):
+    _, meta = golden
+    assert shard_rows(10, 4) == meta["shard_rows"]["10_4"] == oracle.shard_rows(10, 4)
+    assert shard_rows(1, 2) == [1, 0]
+    for m in range(0, 40):
+        for p in (1, 2, 3, 4, 8):
+            assert shard_bounds(m, p) == oracle.shard_bounds(m, p)
+    assert [list(x) for x in partition_heads(8, 4)] == meta["partition_heads_8_4"]
+    with pytest.raises(ConfigError):
+        partition_heads(6, 4)
+
+
+class _Seq:
+    def __init__(self):
+        self.cache = object()
+
+
+def test_policy_and_batch_validation():
+    s = [_Seq() for _ in range(4)]
+    small = Batch(BatchKind.DECODE, [BatchItem(s[0], [1])])
+    at = Batch(BatchKind.DECODE, [BatchItem(x, [1]) for x in s])
+    pol = ShiftPolicy(token_threshold=4)
+    assert choose_mode(pol, small) is ParallelMode.TP
+    assert choose_mode(pol, at) is ParallelMode.SP
+    assert choose_mode(ShiftPolicy.fixed_sp(), small) is ParallelMode.SP
+    assert choose_mode(ShiftPolicy.fixed_tp(), at) is ParallelMode.TP
+    assert default_token_threshold(8) == 32
+    with pytest.raises(ConfigError):
+        ShiftPolicy(token_threshold=0).validate()
+    with pytest.raises(ConfigError):
+        ShiftPolicy(kind="shift").validate()
+    with pytest.raises(ContractViolation):
+        Batch(BatchKind.PREFILL, []).validate()
+    with pytest.raises(ContractViolation):
+        Batch(BatchKind.PREFILL, [BatchItem(s[0], [])]).validate()
+    with pytest.raises(ContractViolation):
+        Batch(BatchKind.DECODE, [BatchItem(s[0], [1, 2])]).validate()
+    Batch(BatchKind.DECODE, [BatchItem(s[0], [1, 2])], speculative=True).validate()
+    with pytest.raises(ContractViolation):
+        Batch(BatchKind.DECODE, [BatchItem(s[0], [1]), BatchItem(s[0], [2])]).validate()
+    assert SwiftKvConfig(True).resolve_cut(4) == 2
+    assert SwiftKvConfig(False).resolve_cut(4) == 4
+    with pytest.raises(ConfigError):
+        SwiftKvConfig(True, 0).resolve_cut(4)
+
+
+@pytest.mark.parametrize("mode", ["tp", "sp"])
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+def test_flop_mirror_matches_oracle(mode, p):
+    ocfg = llama_tiny_config(n_heads=8, n_kv_heads=8 if p == 8 else 4)
+    cfg = product_config(ocfg)
+    for spans, hist, span_logits, cut in [((9, 5), (0, 0), False, None), ((1, 1, 1), (9, 5, 3), False, None),
+                                          ((7, 3), (2, 0), True, None), ((20, 11, 3), (0, 0, 0), False, 2)]:
+        got = flop_count(PassShape(spans, hist, span_logits), mode, cfg, p, swiftkv_cut=cut)
+        want = oracle.flop_count(spans, hist, mode, ocfg, p, span_logits=span_logits, swiftkv_cut=cut)
+        assert got == want
+
+
+def test_rope_and_position_tables_match_oracle_bitexact():
+    from paper_2507_11830_b200.config import LLAMA3_ROPE_SCALING
+    a = rope_table(4096, 128, 500000.0, LLAMA3_ROPE_SCALING)
+    b = rope_tables(4096, 128, 500000.0, LLAMA3_ROPE_SCALING)
+    assert a.tobytes() == b.tobytes()
+    assert sinusoidal_table(64, 256).tobytes() == sinusoidal_positions(np.arange(64), 256,
+                                                                       dtype=np.float32).tobytes()
+
+
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_weight_layouts_are_zero_copy_tp_views(p):
+    """Fused/permuted replica: rank r's q|k|v rows, interleaved gate/up rows and
+    K windows are exactly the reference TP shards (model.py:220-281)."""
+    ocfg = llama_tiny_config(n_kv_heads=4, n_layers=1)
+    ow = init_weights_llama(ocfg, seed=3)
+    w = ModelWeights.from_host(product_config(ocfg), host_dict(ow), p, device="cpu")
+    lw, olw = w.layers[0], ow.layers[0]
+    d, hq, hk = ocfg.head_dim, ocfg.n_heads // p, ocfg.kv_heads // p
+    W = w.qkv_width
+    f = ocfg.ffn_dim // p
+
+    def bf(x):
+        return torch.as_tensor(np.ascontiguousarray(x.T)).to(torch.bfloat16)
+
+    for r in range(p):
+        blk = lw.wqkv[r * W:(r + 1) * W]
+        assert blk.data_ptr() == lw.wqkv.data_ptr() + r * W * ocfg.hidden * 2
+        assert torch.equal(blk[:hq * d], bf(olw["wq"][:, r * hq * d:(r + 1) * hq * d]))
+        assert torch.equal(blk[hq * d:(hq + hk) * d], bf(olw["wk"][:, r * hk * d:(r + 1) * hk * d]))
+        assert torch.equal(blk[(hq + hk) * d:], bf(olw["wv"][:, r * hk * d:(r + 1) * hk * d]))
+        gu = lw.wgu[r * 2 * f:(r + 1) * 2 * f].view(f // 128, 2, 128, -1)
+        assert torch.equal(gu[:, 0].reshape(f, -1), bf(olw["w_gate"][:, r * f:(r + 1) * f]))
+        assert torch.equal(gu[:, 1].reshape(f, -1), bf(olw["w_up"][:, r * f:(r + 1) * f]))
+        assert torch.equal(lw.wdown[:, r * f:(r + 1) * f], bf(olw["w_down"][r * f:(r + 1) * f, :]))
+        assert torch.equal(lw.wo[:, r * hq * d:(r + 1) * hq * d], bf(olw["wo"][r * hq * d:(r + 1) * hq * d, :]))
+
+
+def test_kvcache_bookkeeping_semantics():
+    """Staged vs committed, per-layer cursors, overflow, logical truncate,
+    write counter, fingerprint (reference tests/test_kv_cache.py)."""
+    pool = KvPool(2, ((0, 2), (2, 4)), 8, 16, 4, [0, 1], torch.device("cpu"))
+    c = KvCache(pool, 0, 8)
+    c._stage(0, 0, 3)
+    with pytest.raises(ContractViolation):
+        c.commit(3)
+    for dev, layer in ((0, 1), (1, 0), (1, 1)):
+        c._stage(dev, layer, 3)
+    assert c.token_count == 0
+    c.commit(3)
+    assert c.token_count == 3
+    assert c.device_write_counter(0) == 2 * 3 * 2 * 8 * 2 * 2  # layers*tokens*heads*dim*bf16*(K,V)
+    before = c.write_counter
+    c.truncate(1)
+    assert c.token_count == 1 and c.write_counter == before
+    with pytest.raises(ContractViolation):
+        c.truncate(2)
+    from paper_2507_11830_b200.errors import CacheOverflow
+    with pytest.raises(CacheOverflow):
+        c._stage(0, 0, 9)
+    fp = c.fingerprint()
+    assert fp.axis_order == "layer,head,token,dim" and fp.heads_per_device == 2
+    assert fp.world_size == 2 and fp.precision == "bf16"
+
+
+def test_presets_validate():
+    for cfg, worlds in ((tiny_llama(), (1, 2)), (llama31_8b(), (1, 2, 4, 8)),
+                        (llama33_70b(), (1, 2, 4, 8))):
+        cfg.validate()
+        for p in worlds:
+            cfg.check_world(p)
+    with pytest.raises(ConfigError):
+        tiny_llama().check_world(4)  # 2 kv heads cannot split 4 ways
+    assert llama31_8b().hidden == 4096 and llama33_70b().n_layers == 80
