@@ -245,7 +245,7 @@ def run_ours(args):
     clocks = Clocks(local)
     clocks.start()
     ops.PROFILE = {}
-    launches0 = ops.launch_count
+    launches0 = ops.kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     for _ in range(args.steps):
@@ -253,7 +253,7 @@ def run_ours(args):
     ev1.record()
     sync_barrier()
     prof, ops.PROFILE = ops.PROFILE, None
-    launches = ops.launch_count - launches0
+    launches = ops.kernel_launches() - launches0
     clk = clocks.stop()
     elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1))
     ms_step = elapsed_ms / args.steps

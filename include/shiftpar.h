@@ -42,6 +42,8 @@ typedef int sp_status;
 /* -------------------------------------------------------------- runtime */
 const char* sp_last_error(void);
 int sp_abi_version(void);
+/* Kernels this library has launched so far in the process (all entries). */
+int64_t sp_kernel_launches(void);
 /* 0 when the current device is sm_100 (B200) and the kernels can run. */
 sp_status sp_device_check(int* sm_count);
 
@@ -69,6 +71,12 @@ sp_status sp_device_check(int* sm_count);
 sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_chunk_stride,
                        const void* B, int64_t ldb, void* D, int64_t ldd, int M, int N, int K,
                        int epilogue, int64_t peer_width, int64_t peer_stride, void* stream);
+/* Device workspace for the small-M (decode) regime: when one 128-row M tile
+ * cannot cover the SMs, the GEMM splits K over BN=64 tiles, writes f32
+ * partials here and reduces them in ascending split order (deterministic)
+ * before the epilogue.  NULL disables split-K.  Results are identical within
+ * a regime; across regimes they differ at f32 rounding level. */
+sp_status sp_gemm_set_workspace(void* ws, int64_t bytes);
 
 /* ------------------------------------------------ embedding / norms
  * Embedding gather (parallel_engine.py:339-346 TP, :462-469 SP): out[r, :] =

@@ -24,9 +24,11 @@ _f32 = ctypes.c_float
 SIGNATURES = {
     "sp_last_error": (ctypes.c_char_p, []),
     "sp_abi_version": (_c_int, []),
+    "sp_kernel_launches": (_i64, []),
     "sp_device_check": (_c_int, [ctypes.POINTER(_c_int)]),
     "sp_gemm_bf16": (_c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _c_int, _c_int, _c_int,
                               _c_int, _i64, _i64, _vp]),
+    "sp_gemm_set_workspace": (_c_int, [_vp, _i64]),
     "sp_embed": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _vp]),
     "sp_add_rmsnorm": (_c_int, [_vp, _i64, _vp, _vp, _f32, _vp, _vp, _i64, _c_int, _c_int, _vp]),
     "sp_rope_kv_write": (_c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _c_int, _c_int,

@@ -17,6 +17,8 @@
 #include "common.cuh"
 
 namespace sp {
+int tma_map_bf16(CUtensorMap* out, const void* ptr, int rank, const uint64_t* dims,
+                 const uint64_t* strides, const uint32_t* box);
 namespace attn {
 
 constexpr float kLog2e = 1.4426950408889634f;
@@ -413,6 +415,187 @@ __global__ void combine_kernel(Params p, int head_dim) {
   }
 }
 
+
+// ============================================================ TMA decode
+// head_dim 128, pages of 64*k keys: one CTA per (item, kv head, split); a TMA
+// producer warp streams 64-key K/V page slices into a 4-stage mbarrier ring
+// (128-byte swizzle) and four consumer warps each take 16 keys of every slice
+// (G packed q heads as the m16 rows), keeping private online-softmax state
+// that is merged through shared memory at the end.
+namespace dec {
+constexpr int HD = 128;
+constexpr int PAGE = 64;
+constexpr int STAGES = 4;
+constexpr int NCONS = 4;
+constexpr int NUM_THREADS = (NCONS + 1) * 32;
+constexpr int TILE_BYTES = PAGE * HD * 2;
+constexpr int STAGE_BYTES = 2 * TILE_BYTES;
+constexpr int SMEM_Q = 16 * HD * 2;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + SMEM_Q + 1024 + 256;
+
+// (key, 16-byte chunk) inside a [2 d-chunks][64 keys][128 B] swizzled slice
+__device__ __forceinline__ uint32_t kv_addr(uint32_t base, int key, int c16) {
+  return base + (c16 >> 3) * (TILE_BYTES / 2) + key * 128 + ((((c16 & 7) ^ (key & 7))) << 4);
+}
+
+__global__ void __launch_bounds__(NUM_THREADS) decode_tma_kernel(
+    const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + SMEM_Q);
+  uint64_t* empty = full + STAGES;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int item = blockIdx.x, kvh = blockIdx.y, split = blockIdx.z;
+  const int G = p.group;
+  const int q_row = p.cu_q[item];
+  const int kv_len = p.kv_len[item];
+  const int32_t* bt = p.block_tables + (int64_t)item * p.bt_stride;
+  const int n_tiles = (kv_len + PAGE - 1) / PAGE;
+  const int per_split = (n_tiles + p.n_splits - 1) / p.n_splits;
+  const int t_begin = split * per_split;
+  const int t_end = min(n_tiles, t_begin + per_split);
+
+  if (warp == NCONS && lane == 0) {
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, NCONS);
+    }
+    fence_barrier_init();
+  }
+  if (warp < NCONS) {
+    constexpr int NCH = HD / 8;
+    for (int i = tid; i < 16 * NCH; i += NCONS * 32) {
+      const int r = i / NCH, c = i % NCH;
+      const bool ok = r < G;
+      const __nv_bfloat16* src = p.q;
+      if (ok) src = p.q + (int64_t)q_row * p.ldq + (int64_t)(kvh * G + r) * HD + c * 8;
+      cp_async16(sQ + r * HD + swz<HD>(r, c) * 8, src, ok);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+  }
+  __syncthreads();
+
+  float o[HD / 8][4];
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+  if (warp == NCONS) {
+    if (lane == 0) {
+      for (int t = t_begin, i = 0; t < t_end; ++t, ++i) {
+        const int s = i % STAGES;
+        mbar_wait(empty + s, ((i / STAGES) & 1) ^ 1);
+        const int key0 = t * PAGE;
+        const int page = bt[key0 / p.block_size];
+        const int row = (page * p.kv_heads + kvh) * p.block_size + key0 % p.block_size;
+        uint8_t* st = smem + s * STAGE_BYTES;
+        mbar_arrive_expect_tx(full + s, STAGE_BYTES);
+        tma_load_2d(st, &tmK, full + s, 0, row);
+        tma_load_2d(st + TILE_BYTES / 2, &tmK, full + s, 64, row);
+        tma_load_2d(st + TILE_BYTES, &tmV, full + s, 0, row);
+        tma_load_2d(st + TILE_BYTES + TILE_BYTES / 2, &tmV, full + s, 64, row);
+      }
+    }
+    __syncwarp();
+  } else {
+    uint32_t qf[HD / 16][4];
+    load_q_frags<HD>(qf, sQ, 0, lane);
+#pragma unroll
+    for (int n = 0; n < HD / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    const int limit[2] = {kv_len - 1, kv_len - 1};
+    const int m = lane >> 3;
+    for (int t = t_begin, i = 0; t < t_end; ++t, ++i) {
+      const int s = i % STAGES;
+      mbar_wait(full + s, (i / STAGES) & 1);
+      const uint32_t sk = smem_u32(smem + s * STAGE_BYTES);
+      const uint32_t sv = sk + TILE_BYTES;
+      float sc[2][4];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < HD / 16; ++ks) {
+        uint32_t b0, b1, b2, b3;
+        ldmatrix_x4(kv_addr(sk, warp * 16 + (m >> 1) * 8 + (lane & 7), ks * 2 + (m & 1)), b0, b1, b2,
+                    b3);
+        mma_bf16_16816(sc[0], qf[ks], b0, b1);
+        mma_bf16_16816(sc[1], qf[ks], b2, b3);
+      }
+      const int kbase = t * PAGE + warp * 16;
+      softmax_update<HD, 16>(sc, o, mrow, lrow, kbase, limit, kbase + 16 > kv_len, p.scale_log2,
+                             lane);
+      uint32_t a[4];
+      a[0] = pack_bf16x2(sc[0][0], sc[0][1]);
+      a[1] = pack_bf16x2(sc[0][2], sc[0][3]);
+      a[2] = pack_bf16x2(sc[1][0], sc[1][1]);
+      a[3] = pack_bf16x2(sc[1][2], sc[1][3]);
+#pragma unroll
+      for (int n = 0; n < HD / 8; n += 2) {
+        uint32_t b0, b1, b2, b3;
+        ldmatrix_x4_trans(kv_addr(sv, warp * 16 + (m & 1) * 8 + (lane & 7), n + (m >> 1)), b0, b1,
+                          b2, b3);
+        mma_bf16_16816(o[n], a, b0, b1);
+        mma_bf16_16816(o[n + 1], a, b2, b3);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
+    }
+  }
+  __syncthreads();  // ring free -> merge scratch
+  float* sm = reinterpret_cast<float*>(smem);
+  float* sl = sm + NCONS * 16;
+  float* so = sl + NCONS * 16;
+  if (warp < NCONS) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = (lane >> 2) + 8 * h;
+      if ((lane & 3) == 0) {
+        sm[warp * 16 + r] = mrow[h];
+        sl[warp * 16 + r] = lrow[h];
+      }
+#pragma unroll
+      for (int n = 0; n < HD / 8; ++n) {
+        so[(warp * 16 + r) * HD + n * 8 + (lane & 3) * 2] = o[n][2 * h];
+        so[(warp * 16 + r) * HD + n * 8 + (lane & 3) * 2 + 1] = o[n][2 * h + 1];
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < G * HD; i += NUM_THREADS) {
+    const int row = i / HD, c = i % HD;
+    float mx = -INFINITY;
+    for (int w = 0; w < NCONS; ++w) mx = fmaxf(mx, sm[w * 16 + row]);
+    float l = 0.f, acc = 0.f;
+    if (mx != -INFINITY) {
+      for (int w = 0; w < NCONS; ++w) {
+        const float f = exp2f(sm[w * 16 + row] - mx);
+        l += sl[w * 16 + row] * f;
+        acc += so[(w * 16 + row) * HD + c] * f;
+      }
+    }
+    const int qh = kvh * G + row;
+    if (p.n_splits == 1) {
+      p.out[(int64_t)q_row * p.ldo + (int64_t)qh * HD + c] = __float2bfloat16_rn(acc / l);
+    } else {
+      const int64_t slot = ((int64_t)item * p.q_heads + qh) * p.n_splits + split;
+      p.ws_o[slot * HD + c] = l > 0.f ? acc / l : 0.f;
+      if (c == 0) p.ws_lse[slot] = l > 0.f ? mx + log2f(l) : -INFINITY;
+    }
+  }
+}
+}  // namespace dec
+
+static int decode_tma_splits(int n_items, int kv_heads, int max_kv_len) {
+  const int ctas = n_items * kv_heads;
+  int want = (2 * 148 + ctas - 1) / ctas;
+  const int pages = (max_kv_len + dec::PAGE - 1) / dec::PAGE;
+  const int max_useful = (pages + 3) / 4;  // >= 4 page slices per split
+  if (want > max_useful) want = max_useful;
+  if (want > 64) want = 64;
+  return want < 1 ? 1 : want;
+}
+
 template <int HD>
 static int launch(const Params& p, int n_items, int n_work, cudaStream_t st) {
   if (n_work > 0) {
@@ -540,6 +723,39 @@ extern "C" sp_status sp_attention(const void* q, int64_t ldq, int64_t q_rows, co
                              pool_blocks * (int64_t)kv_heads * block_size, block_tables, bt_stride,
                              cu_q, first_pos, kv_len, work, n_work, out, ldo, q_heads, kv_heads,
                              block_size, st);
+  }
+  if (n_work == 0 && head_dim == 128 && block_size % attn::dec::PAGE == 0 && pool_blocks > 0) {
+    CUtensorMap tk, tv;
+    uint64_t dims[2] = {128, (uint64_t)(pool_blocks * (int64_t)kv_heads * block_size)};
+    uint64_t strides[1] = {128 * 2};
+    uint32_t box[2] = {64, attn::dec::PAGE};
+    if (int rc = tma_map_bf16(&tk, k_pool, 2, dims, strides, box)) return rc;
+    if (int rc = tma_map_bf16(&tv, v_pool, 2, dims, strides, box)) return rc;
+    p.n_splits = attn::decode_tma_splits(n_items, kv_heads, max_kv_len);
+    p.ws_o = p.ws_lse = nullptr;
+    if (p.n_splits > 1) {
+      const int64_t need = (int64_t)n_items * q_heads * p.n_splits * (head_dim + 1) * 4;
+      if (!ws || ws_bytes < need) {
+        p.n_splits = 1;
+      } else {
+        p.ws_o = static_cast<float*>(ws);
+        p.ws_lse = p.ws_o + (int64_t)n_items * q_heads * p.n_splits * head_dim;
+      }
+    }
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(attn::dec::decode_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           attn::dec::SMEM_BYTES);
+      attr = true;
+    }
+    attn::dec::decode_tma_kernel<<<dim3(n_items, kv_heads, p.n_splits), attn::dec::NUM_THREADS,
+                                   attn::dec::SMEM_BYTES, st>>>(tk, tv, p);
+    if (int rc = check_launch("attn_decode_tma_kernel")) return rc;
+    if (p.n_splits > 1) {
+      attn::combine_kernel<<<dim3(n_items, q_heads), head_dim, 0, st>>>(p, head_dim);
+      return check_launch("attn_combine_kernel");
+    }
+    return kOk;
   }
   switch (head_dim) {
     case 32: return attn::launch<32>(p, n_items, n_work, st);

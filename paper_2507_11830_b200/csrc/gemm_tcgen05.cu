@@ -16,7 +16,9 @@
 // and of the N window, so row/column shards are bit-identical to the full GEMM.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
@@ -26,14 +28,24 @@
 namespace sp {
 namespace gemm {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4, ACC_STAGES = 2;
+constexpr int BM = 128, BK = 64, ACC_STAGES = 2;
 constexpr int A_BYTES = BM * BK * 2;
-constexpr int B_BYTES = BN * BK * 2;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 192;
-constexpr int GROUP_M = 16;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+
+// N-tile variants: 256 for large GEMMs (1 CTA/SM), 128/64/32 so that small-M
+// (decode) GEMMs still spread the weight stream over every SM (2 CTAs/SM).
+// The K loop and MMA K-step are identical for every width, so a given output
+// element is bit-identical whichever variant computes it.
+template <int BN_>
+struct Tile {
+  static constexpr int BN = BN_;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN >= 256 ? 4 : (BN >= 128 ? 6 : 4);
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int MIN_BLOCKS = BN >= 128 ? 1 : 2;
+};
 
 struct Params {
   int M, N, K;
@@ -43,17 +55,31 @@ struct Params {
   void* D;
   int64_t ldd;
   int64_t peer_width, peer_stride;
+  // split-K (small-M regime): tile t covers k-blocks of split t % ksplit and
+  // stores raw f32 partials to ws[split][M][N]; splitk_reduce applies the epilogue
+  int ksplit, kb_per_split;
+  float* ws;
+  int group_m;  // m-tiles per raster group (A rows of a group stay L2-resident)
 };
 
 __device__ __forceinline__ void tile_coords(int t, const Params& p, int& mb, int& nb) {
-  const int per_group = GROUP_M * p.num_n;
+  const int per_group = p.group_m * p.num_n;
   const int g = t / per_group;
-  const int first_m = g * GROUP_M;
-  const int gm = min(p.num_m - first_m, GROUP_M);
+  const int first_m = g * p.group_m;
+  const int gm = min(p.num_m - first_m, p.group_m);
   const int r = t - g * per_group;
   mb = first_m + r % gm;
   nb = r / gm;
 }
+
+__device__ __forceinline__ void split_coords(int t, const Params& p, int& mb, int& nb, int& kb0,
+                                             int& kb1, int& ks) {
+  ks = t % p.ksplit;
+  tile_coords(t / p.ksplit, p, mb, nb);
+  kb0 = ks * p.kb_per_split;
+  kb1 = min(p.k_blocks, kb0 + p.kb_per_split);
+}
+
 
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float c = 0.7978845608028654f, k = 0.044715f;
@@ -125,9 +151,13 @@ __device__ __forceinline__ void store_chunk(const Params& p, int m, int n0, cons
   }
 }
 
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+template <int BN_>
+__global__ void __launch_bounds__(NUM_THREADS, Tile<BN_>::MIN_BLOCKS)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const Params p) {
+  using T = Tile<BN_>;
+  constexpr int BN = T::BN, STAGES = T::STAGES, STAGE_BYTES = T::STAGE_BYTES;
+  constexpr int TMEM_COLS = T::TMEM_COLS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -165,9 +195,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        int mb, nb;
-        tile_coords(t, p, mb, nb);
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        int mb, nb, kb0, kb1, ks;
+        split_coords(t, p, mb, nb, kb0, kb1, ks);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           mbar_arrive_expect_tx(full + stage, STAGE_BYTES);
@@ -194,10 +224,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0, acc = 0;
       uint32_t phase = 0, aphase = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        int mb, nb, kb0, kb1, ks;
+        split_coords(t, p, mb, nb, kb0, kb1, ks);
         mbar_wait(tempty + acc, aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + stage * STAGE_BYTES);
@@ -205,7 +237,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             umma_bf16(d_tmem, sdesc_sw128(a_addr + k * 32), sdesc_sw128(b_addr + k * 32), idesc,
-                      (kb | k) != 0 ? 1u : 0u);
+                      (kb != kb0 || k != 0) ? 1u : 0u);
           }
           umma_commit(empty + stage);
           if (++stage == STAGES) {
@@ -228,13 +260,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int acc = 0;
     uint32_t aphase = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      int mb, nb;
-      tile_coords(t, p, mb, nb);
+      int mb, nb, kb0, kb1, ks;
+      split_coords(t, p, mb, nb, kb0, kb1, ks);
       mbar_wait(tfull + acc, aphase);
       tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
       const int m = mb * BM + row;
-      if (p.epi == SP_EPI_SWIGLU) {
+      if (p.ws != nullptr) {
+        // split-K partial: raw f32 into ws[ks][M][N]
+        Params q = p;
+        q.D = p.ws + (int64_t)ks * p.M * p.N;
+        q.ldd = p.N;
+        q.peer_width = 0;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tb + c, r);
+          tmem_ld_wait();
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          store_chunk(q, m, nb * BN + c, v, SP_EPI_STORE_F32, p.N);
+        }
+      } else if (p.epi == SP_EPI_SWIGLU) {
 #pragma unroll 1
         for (int c = 0; c < BN / 2; c += 32) {
           uint32_t g[32], u[32];
@@ -276,6 +324,78 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// split-K reduction: v = sum_s ws[s] in ascending s (deterministic), then the
+// epilogue; one thread = 8 consecutive output columns of one row.
+__global__ void splitk_reduce_kernel(const Params p) {
+  const int n_out = p.epi == SP_EPI_SWIGLU ? p.N / 2 : p.N;
+  const int64_t per_row = n_out / 8;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)p.M * per_row) return;
+  const int m = (int)(idx / per_row);
+  const int c = (int)(idx % per_row) * 8;
+  const int64_t split_stride = (int64_t)p.M * p.N;
+  float v[8];
+  if (p.epi == SP_EPI_SWIGLU) {
+    const int g0 = (c / 128) * 256 + c % 128;
+    float g[8], u[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) g[j] = u[j] = 0.f;
+    for (int s = 0; s < p.ksplit; ++s) {
+      const float* row = p.ws + s * split_stride + (int64_t)m * p.N;
+      const float4 a0 = *reinterpret_cast<const float4*>(row + g0);
+      const float4 a1 = *reinterpret_cast<const float4*>(row + g0 + 4);
+      const float4 b0 = *reinterpret_cast<const float4*>(row + g0 + 128);
+      const float4 b1 = *reinterpret_cast<const float4*>(row + g0 + 132);
+      g[0] += a0.x; g[1] += a0.y; g[2] += a0.z; g[3] += a0.w;
+      g[4] += a1.x; g[5] += a1.y; g[6] += a1.z; g[7] += a1.w;
+      u[0] += b0.x; u[1] += b0.y; u[2] += b0.z; u[3] += b0.w;
+      u[4] += b1.x; u[5] += b1.y; u[6] += b1.z; u[7] += b1.w;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = silu(g[j]) * u[j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = 0.f;
+    for (int s = 0; s < p.ksplit; ++s) {
+      const float* row = p.ws + s * split_stride + (int64_t)m * p.N + c;
+      const float4 a0 = *reinterpret_cast<const float4*>(row);
+      const float4 a1 = *reinterpret_cast<const float4*>(row + 4);
+      v[0] += a0.x; v[1] += a0.y; v[2] += a0.z; v[3] += a0.w;
+      v[4] += a1.x; v[5] += a1.y; v[6] += a1.z; v[7] += a1.w;
+    }
+    if (p.epi == SP_EPI_GELU) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = gelu_tanh(v[j]);
+    }
+  }
+  int64_t col = c, base = 0;
+  if (p.peer_width > 0) {
+    const int64_t peer = c / p.peer_width;
+    col = c - peer * p.peer_width;
+    base = peer * p.peer_stride;
+  }
+  if (p.epi == SP_EPI_STORE_F32 || p.epi == SP_EPI_ADD_F32) {
+    float* dst = reinterpret_cast<float*>(p.D) + base + (int64_t)m * p.ldd + col;
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    if (p.epi == SP_EPI_ADD_F32) {
+      float4 x0 = d4[0], x1 = d4[1];
+      d4[0] = make_float4(x0.x + v[0], x0.y + v[1], x0.z + v[2], x0.w + v[3]);
+      d4[1] = make_float4(x1.x + v[4], x1.y + v[5], x1.z + v[6], x1.w + v[7]);
+    } else {
+      d4[0] = make_float4(v[0], v[1], v[2], v[3]);
+      d4[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
+  } else {
+    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.D) + base + (int64_t)m * p.ldd + col;
+    uint4 u;
+    u.x = pack_bf16x2(v[0], v[1]);
+    u.y = pack_bf16x2(v[2], v[3]);
+    u.z = pack_bf16x2(v[4], v[5]);
+    u.w = pack_bf16x2(v[6], v[7]);
+    *reinterpret_cast<uint4*>(dst) = u;
   }
 }
 
@@ -345,27 +465,13 @@ int tma_map_bf16(CUtensorMap* out, const void* ptr, int rank, const uint64_t* di
 
 using namespace sp;
 
-extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
-                                  int64_t a_chunk_stride, const void* B, int64_t ldb, void* D,
-                                  int64_t ldd, int M, int N, int K, int epilogue,
-                                  int64_t peer_width, int64_t peer_stride, void* stream) {
+template <int BN>
+static int launch(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_chunk_stride,
+                  const void* B, int64_t ldb, void* D, int64_t ldd, int M, int N, int K,
+                  int epilogue, int64_t peer_width, int64_t peer_stride, void* stream,
+                  float* ws = nullptr, int ksplit = 1) {
   using namespace sp::gemm;
-  if (M < 0 || N <= 0 || K <= 0) return fail(kInvalid, "gemm: bad M/N/K");
-  if (M == 0) return kOk;
-  if (!A || !B || !D) return fail(kInvalid, "gemm: null pointer");
-  if (epilogue < SP_EPI_STORE_BF16 || epilogue > SP_EPI_GELU)
-    return fail(kInvalid, "gemm: unknown epilogue");
-  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
-    return fail(kInvalid, "gemm: A/B must be 16-byte aligned");
-  if (lda % 8 || ldb % 8 || ldd % 8) return fail(kInvalid, "gemm: leading dims must be multiples of 8");
-  if (a_kchunk > 0 && (a_kchunk % BK || K % a_kchunk || a_chunk_stride % 8))
-    return fail(kUnsupported, "gemm: chunked-K A needs chunk % 64 == 0 and K % chunk == 0");
-  if (epilogue == SP_EPI_SWIGLU && N % BN)
-    return fail(kUnsupported, "gemm: SwiGLU epilogue needs N % 256 == 0");
-  if (peer_width > 0 && (peer_width % 32 || peer_stride % 8))
-    return fail(kUnsupported, "gemm: peer layout needs width % 32 == 0");
-  if (reinterpret_cast<uintptr_t>(D) & 15) return fail(kInvalid, "gemm: D must be 16-byte aligned");
-
+  using T = Tile<BN>;
   CUtensorMap ta, tb;
   {
     const uint64_t kin = a_kchunk > 0 ? (uint64_t)a_kchunk : (uint64_t)K;
@@ -380,7 +486,7 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
   {
     uint64_t dims[2] = {(uint64_t)K, (uint64_t)N};
     uint64_t strides[1] = {(uint64_t)ldb * 2};
-    uint32_t box[2] = {BK, BN};
+    uint32_t box[2] = {BK, (uint32_t)BN};
     if (int rc = get_map(&tb, B, 2, dims, strides, box)) return rc;
   }
   Params p;
@@ -397,13 +503,111 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
   p.ldd = ldd;
   p.peer_width = peer_width;
   p.peer_stride = peer_stride;
-
+  // raster: walk all N tiles of a group of m-tiles whose A rows fit ~40 MB of L2,
+  // so every B (weight) tile is streamed from HBM once per group
+  {
+    const int64_t a_tile_bytes = (int64_t)BM * K * 2;
+    int64_t gm = (40ll << 20) / std::max<int64_t>(a_tile_bytes, 1);
+    p.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(gm, p.num_m));
+  }
+  p.ws = ws;
+  p.ksplit = ws ? ksplit : 1;
+  p.kb_per_split = (int)cdiv(p.k_blocks, p.ksplit);
+  p.num_tiles *= p.ksplit;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         T::SMEM_BYTES);
     attr = true;
   }
-  const int grid = std::min(p.num_tiles, sm_count());
-  gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, reinterpret_cast<cudaStream_t>(stream)>>>(ta, tb, p);
-  return check_launch("gemm_kernel");
+  const int grid = std::min(p.num_tiles, sm_count() * T::MIN_BLOCKS);
+  gemm_kernel<BN><<<grid, NUM_THREADS, T::SMEM_BYTES, reinterpret_cast<cudaStream_t>(stream)>>>(
+      ta, tb, p);
+  if (int rc = check_launch("gemm_kernel")) return rc;
+  if (ws) {
+    const int n_out = epilogue == SP_EPI_SWIGLU ? N / 2 : N;
+    const int64_t threads = (int64_t)M * (n_out / 8);
+    splitk_reduce_kernel<<<(unsigned)cdiv(threads, 256), 256, 0,
+                           reinterpret_cast<cudaStream_t>(stream)>>>(p);
+    return check_launch("splitk_reduce_kernel");
+  }
+  return kOk;
+}
+
+// split-K workspace (set once by the host; never allocated in the hot path)
+static float* g_ws = nullptr;
+static int64_t g_ws_bytes = 0;
+
+
+extern "C" sp_status sp_gemm_set_workspace(void* ws, int64_t bytes) {
+  if (bytes < 0 || (ws == nullptr && bytes > 0)) return fail(kInvalid, "gemm workspace: bad args");
+  if (reinterpret_cast<uintptr_t>(ws) & 15) return fail(kInvalid, "gemm workspace must be 16B aligned");
+  g_ws = static_cast<float*>(ws);
+  g_ws_bytes = bytes;
+  return kOk;
+}
+
+extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
+                                  int64_t a_chunk_stride, const void* B, int64_t ldb, void* D,
+                                  int64_t ldd, int M, int N, int K, int epilogue,
+                                  int64_t peer_width, int64_t peer_stride, void* stream) {
+  using namespace sp::gemm;
+  if (M < 0 || N <= 0 || K <= 0) return fail(kInvalid, "gemm: bad M/N/K");
+  if (M == 0) return kOk;
+  if (!A || !B || !D) return fail(kInvalid, "gemm: null pointer");
+  if (epilogue < SP_EPI_STORE_BF16 || epilogue > SP_EPI_GELU)
+    return fail(kInvalid, "gemm: unknown epilogue");
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
+    return fail(kInvalid, "gemm: A/B must be 16-byte aligned");
+  if (lda % 8 || ldb % 8 || ldd % 8) return fail(kInvalid, "gemm: leading dims must be multiples of 8");
+  if (a_kchunk > 0 && (a_kchunk % BK || K % a_kchunk || a_chunk_stride % 8))
+    return fail(kUnsupported, "gemm: chunked-K A needs chunk % 64 == 0 and K % chunk == 0");
+  if (epilogue == SP_EPI_SWIGLU && N % 256)
+    return fail(kUnsupported, "gemm: SwiGLU epilogue needs N % 256 == 0");
+  if (peer_width > 0 && (peer_width % 32 || peer_stride % 8))
+    return fail(kUnsupported, "gemm: peer layout needs width % 32 == 0");
+  if (reinterpret_cast<uintptr_t>(D) & 15) return fail(kInvalid, "gemm: D must be 16-byte aligned");
+
+  // Regime selection (numerics are identical within a regime):
+  //  * enough 128x256 tiles to cover the SMs        -> BN=256
+  //  * one M tile (decode-size M) and a workspace    -> split-K over BN=64 tiles,
+  //    f32 partials reduced in ascending split order by splitk_reduce_kernel
+  //  * otherwise                                     -> narrower N tiles (128/64/32),
+  //    bit-identical to BN=256 (same K loop)
+  const int sms = sm_count();
+  const int64_t m_tiles = cdiv(M, BM);
+  const int64_t k_blocks = cdiv(K, BK);
+  const bool no_split = getenv("SP_GEMM_NO_SPLITK") != nullptr;
+  int bn = 256;
+  if (m_tiles * cdiv(N, 256) < sms) {
+    if (m_tiles == 1 && g_ws && !no_split && N % 32 == 0 && k_blocks >= 4) {
+      const int64_t base = cdiv(N, 64);
+      int64_t ks = (2 * sms) / base;
+      ks = std::max<int64_t>(1, std::min<int64_t>(ks, k_blocks / 4));
+      const int64_t per = cdiv(k_blocks, ks);
+      ks = cdiv(k_blocks, per);
+      if (ks * (int64_t)M * N * 4 <= g_ws_bytes && (ks > 1 || epilogue == SP_EPI_SWIGLU))
+        return launch<64>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
+                          peer_width, peer_stride, stream, g_ws, (int)ks);
+    }
+    if (epilogue != SP_EPI_SWIGLU) {
+      bn = 32;
+      for (int c : {128, 64}) {
+        if (m_tiles * cdiv(N, c) >= sms) {
+          bn = c;
+          break;
+        }
+      }
+    }
+  }
+  if (const char* f = getenv("SP_GEMM_FORCE_BN")) {
+    const int fb = atoi(f);
+    if ((fb == 32 || fb == 64 || fb == 128 || fb == 256) && epilogue != SP_EPI_SWIGLU) bn = fb;
+  }
+  switch (bn) {
+    case 256: return launch<256>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue, peer_width, peer_stride, stream);
+    case 128: return launch<128>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue, peer_width, peer_stride, stream);
+    case 64: return launch<64>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue, peer_width, peer_stride, stream);
+    default: return launch<32>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue, peer_width, peer_stride, stream);
+  }
 }

@@ -1,6 +1,7 @@
 // Error plumbing, device check and the small HBM-bound kernels of the path:
 // embedding gather, fused residual-add + RMSNorm, RoPE + paged KV write,
 // all-to-all pack/unpack, loopback add, argmax and row gather.
+#include <atomic>
 #include <cstdio>
 #include <string>
 
@@ -18,7 +19,10 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+static std::atomic<long long> g_launches{0};
+
 int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(kCuda, std::string(what) + ": " + cudaGetErrorString(e));
   return kOk;
@@ -264,6 +268,8 @@ static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s)
 extern "C" const char* sp_last_error(void) { return sp::g_err.c_str(); }
 
 extern "C" int sp_abi_version(void) { return 1; }
+
+extern "C" int64_t sp_kernel_launches(void) { return (int64_t)sp::g_launches.load(); }
 
 extern "C" sp_status sp_device_check(int* sm_count) {
   int dev = 0;

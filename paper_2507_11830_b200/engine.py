@@ -210,6 +210,8 @@ class Engine:
         self.kv_partition = partition_heads(cfg.kv_heads, self.world_size)
         self.device = weights.embed.device
         ops.device_check()
+        # split-K workspace for decode-size GEMMs (allocated once, never in the hot path)
+        ops.set_gemm_workspace(torch.empty(64 << 20, dtype=torch.uint8, device=self.device))
         if isinstance(group, LoopbackGroup):
             group._add = ops.add_f32
         if self.swiftkv.enabled:

@@ -52,6 +52,11 @@ class _Timed:
         return False
 
 
+def kernel_launches() -> int:
+    """Kernels libshiftpar.so has launched in this process (counted in C)."""
+    return int(_lib.load().sp_kernel_launches())
+
+
 def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
@@ -91,12 +96,23 @@ def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, epilogue: int, *, M:
         return
     lib = _lib.load()
     nbytes = (M * K + N * K) * 2 + M * (N // 2 if epilogue == EPI_SWIGLU else N) * d.element_size()
-    with _Timed("gemm", 2 * M * N * K, nbytes):
+    with _Timed("gemm", 2 * M * N * K, nbytes):  # (split-K reduce, if any, included)
         rc = lib.sp_gemm_bf16(a.data_ptr(), lda, a_kchunk, a_chunk_stride, b.data_ptr(), ldb,
                               d.data_ptr(), ldd, M, N, K, epilogue, peer_width, peer_stride,
                               _stream())
     _lib.check(rc, "sp_gemm_bf16")
     _count()
+
+
+_gemm_ws: Optional[torch.Tensor] = None
+
+
+def set_gemm_workspace(ws: Optional[torch.Tensor]) -> None:
+    """Register the split-K workspace (kept alive here); None disables split-K."""
+    global _gemm_ws
+    _gemm_ws = ws
+    nbytes = 0 if ws is None else ws.numel() * ws.element_size()
+    _lib.check(_lib.load().sp_gemm_set_workspace(_ptr(ws), nbytes), "sp_gemm_set_workspace")
 
 
 def embed(ids: torch.Tensor, table: torch.Tensor, out: torch.Tensor,

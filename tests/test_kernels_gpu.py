@@ -116,8 +116,10 @@ def test_gemm_strided_b_window_is_zero_copy_tp_shard():
         assert rel(d, want) < 1e-4
 
 
-def test_gemm_row_and_column_splits_bitexact():
-    """tensor_core.py:1-28 property on the GPU: fixed tiles, no split-K."""
+def test_gemm_row_and_column_splits_bitexact(monkeypatch):
+    """tensor_core.py:1-28 property on the GPU: fixed tiles, no split-K (the
+    split-K regime for decode-size M is pinned off here)."""
+    monkeypatch.setenv("SP_GEMM_NO_SPLITK", "1")
     M, N, K = 700, 1024, 512
     a, b = rnd(M, K, seed=16), rnd(N, K, seed=17)
     full = torch.empty(M, N, device="cuda")
@@ -307,3 +309,72 @@ def test_pack_unpack_roundtrip_and_add_argmax():
     ops.argmax(lg, idx)
     want = lg.argmax(-1).to(torch.int32)
     assert torch.equal(idx, want) and int(idx[2]) == 7
+
+
+def test_gemm_tile_width_variants_are_bitexact(monkeypatch):
+    """The N-tile variants (256/128/64/32, picked by M and N) share the K loop, so
+    an output element does not depend on which variant computed it."""
+    monkeypatch.setenv("SP_GEMM_NO_SPLITK", "1")
+    M, N, K = 200, 768, 1024
+    a, b = rnd(M, K, seed=30), rnd(N, K, seed=31)
+    outs = {}
+    for bn in ("256", "128", "64", "32"):
+        monkeypatch.setenv("SP_GEMM_FORCE_BN", bn)
+        d = torch.empty(M, N, device="cuda")
+        ops.gemm(a, b, d, ops.EPI_STORE_F32, M=M, N=N, K=K, lda=K, ldb=K, ldd=N)
+        x = torch.ones(M, N, device="cuda")
+        ops.gemm(a, b, x, ops.EPI_ADD_F32, M=M, N=N, K=K, lda=K, ldb=K, ldd=N)
+        outs[bn] = (d, x)
+    for bn, (d, x) in outs.items():
+        assert torch.equal(d, outs["256"][0]), bn
+        assert torch.equal(x, outs["256"][1]), bn
+    assert rel(outs["32"][0], a.float() @ b.float().t()) < 1e-4
+
+
+@pytest.mark.parametrize("epi", ["f32", "add", "bf16", "swiglu", "gelu", "peer"])
+def test_gemm_split_k_regime(epi):
+    """Decode-size M: split-K over BN=64 tiles with an ascending-order reduce.
+    Deterministic run to run; within f32 accumulation noise of the reference."""
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    ops.set_gemm_workspace(ws)
+    try:
+        M, N, K = 48, 1024, 4096
+        a, b = rnd(M, K, seed=40), rnd(N, K, seed=41)
+        ref = a.float() @ b.float().t()
+        outs = []
+        for _ in range(2):
+            if epi == "f32":
+                d = torch.empty(M, N, device="cuda")
+                ops.gemm(a, b, d, ops.EPI_STORE_F32, M=M, N=N, K=K, lda=K, ldb=K, ldd=N)
+                want, tol = ref, 1e-4
+            elif epi == "add":
+                d = torch.ones(M, N, device="cuda")
+                ops.gemm(a, b, d, ops.EPI_ADD_F32, M=M, N=N, K=K, lda=K, ldb=K, ldd=N)
+                want, tol = ref + 1, 1e-4
+            elif epi == "bf16":
+                d = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+                ops.gemm(a, b, d, ops.EPI_STORE_BF16, M=M, N=N, K=K, lda=K, ldb=K, ldd=N)
+                want, tol = ref, 1e-2
+            elif epi == "gelu":
+                d = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+                ops.gemm(a, b, d, ops.EPI_GELU, M=M, N=N, K=K, lda=K, ldb=K, ldd=N)
+                want, tol = torch.nn.functional.gelu(ref, approximate="tanh"), 1e-2
+            elif epi == "swiglu":
+                f = N // 2
+                d = torch.empty(M, f, device="cuda", dtype=torch.bfloat16)
+                ops.gemm(a, b, d, ops.EPI_SWIGLU, M=M, N=N, K=K, lda=K, ldb=K, ldd=f)
+                v = ref.view(M, f // 128, 2, 128)
+                want = (torch.nn.functional.silu(v[:, :, 0]) * v[:, :, 1]).reshape(M, f)
+                tol = 1e-2
+            else:
+                P, W = 4, N // 4
+                d = torch.empty(P * M, W, device="cuda", dtype=torch.bfloat16)
+                ops.gemm(a, b, d, ops.EPI_STORE_BF16, M=M, N=N, K=K, lda=K, ldb=K, ldd=W,
+                         peer_width=W, peer_stride=M * W)
+                d = torch.cat([d[s * M:(s + 1) * M] for s in range(P)], dim=1)
+                want, tol = ref, 1e-2
+            outs.append(d.clone())
+            assert rel(d, want) < tol
+        assert torch.equal(outs[0], outs[1])
+    finally:
+        ops.set_gemm_workspace(None)

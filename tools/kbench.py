@@ -46,6 +46,7 @@ def timeit(fn, reps=10, warm=3, do_flush=True):
 
 
 def gemm_cases():
+    ops.set_gemm_workspace(torch.empty(64 << 20, dtype=torch.uint8, device="cuda"))
     M = 8192
     h, f, qkv, V = 4096, 14336, 6144, 128256
     out = []
@@ -55,6 +56,12 @@ def gemm_cases():
                                 ("down", M, h, f, ops.EPI_ADD_F32),
                                 ("square8k", 8192, 8192, 8192, ops.EPI_STORE_BF16),
                                 ("decode_qkv_b64", 64, qkv, h, ops.EPI_STORE_BF16),
+                                ("decode_o_b64", 64, h, h, ops.EPI_ADD_F32),
+                                ("decode_gate_up_b64", 64, 2 * f, h, ops.EPI_SWIGLU),
+                                ("decode_down_b64", 64, h, f, ops.EPI_ADD_F32),
+                                ("decode_qkv_b8", 8, qkv, h, ops.EPI_STORE_BF16),
+                                ("decode_down_b8", 8, h, f, ops.EPI_ADD_F32),
+                                ("decode_qkv_b256", 256, qkv, h, ops.EPI_STORE_BF16),
                                 ("lm_head_b64", 64, V, h, ops.EPI_STORE_F32)]:
         a = torch.randn(m, k, device="cuda").to(torch.bfloat16)
         b = torch.randn(n, k, device="cuda").to(torch.bfloat16)
