@@ -190,6 +190,8 @@ constexpr int PF_KT = 64;
 
 template <int HD>
 __global__ void __launch_bounds__(PF_WARPS * 32) prefill_kernel(Params p) {
+  pdl_wait();  // inputs of this kernel are written by its predecessor
+  pdl_trigger();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw);
   __nv_bfloat16* sK = sQ + PF_ROWS * HD;        // [2][KT][HD]
@@ -286,6 +288,8 @@ constexpr int DC_KT = 32;
 
 template <int HD>
 __global__ void __launch_bounds__(DC_WARPS * 32) decode_kernel(Params p) {
+  pdl_wait();  // inputs of this kernel are written by its predecessor
+  pdl_trigger();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(smem_raw) + warp * (4 * DC_KT * HD);
@@ -397,6 +401,8 @@ __global__ void __launch_bounds__(DC_WARPS * 32) decode_kernel(Params p) {
 }
 
 __global__ void combine_kernel(Params p, int head_dim) {
+  pdl_wait();  // inputs of this kernel are written by its predecessor
+  pdl_trigger();
   const int item = blockIdx.x, qh = blockIdx.y;
   const int64_t base = ((int64_t)item * p.q_heads + qh) * p.n_splits;
   float mx = -INFINITY;
@@ -440,6 +446,8 @@ __device__ __forceinline__ uint32_t kv_addr(uint32_t base, int key, int c16) {
 
 __global__ void __launch_bounds__(NUM_THREADS) decode_tma_kernel(
     const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Params p) {
+  pdl_wait();  // inputs of this kernel are written by its predecessor
+  pdl_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -605,7 +613,7 @@ static int launch(const Params& p, int n_items, int n_work, cudaStream_t st) {
       cudaFuncSetAttribute(prefill_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       attr = true;
     }
-    prefill_kernel<HD><<<dim3(n_work, p.kv_heads), PF_WARPS * 32, smem, st>>>(p);
+    launch_k(prefill_kernel<HD>, dim3(n_work, p.kv_heads), PF_WARPS * 32, smem, st, p);
     return check_launch("attn_prefill_kernel");
   }
   const int smem_tiles = (DC_WARPS * 4 * DC_KT * HD + 16 * HD) * 2;
@@ -616,10 +624,10 @@ static int launch(const Params& p, int n_items, int n_work, cudaStream_t st) {
     cudaFuncSetAttribute(decode_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  decode_kernel<HD><<<dim3(n_items, p.kv_heads, p.n_splits), DC_WARPS * 32, smem, st>>>(p);
+  launch_k(decode_kernel<HD>, dim3(n_items, p.kv_heads, p.n_splits), DC_WARPS * 32, smem, st, p);
   if (int rc = check_launch("attn_decode_kernel")) return rc;
   if (p.n_splits > 1) {
-    combine_kernel<<<dim3(n_items, p.q_heads), HD, 0, st>>>(p, HD);
+    launch_k(combine_kernel, dim3(n_items, p.q_heads), HD, 0, st, p, HD);
     return check_launch("attn_combine_kernel");
   }
   return kOk;
@@ -748,11 +756,10 @@ extern "C" sp_status sp_attention(const void* q, int64_t ldq, int64_t q_rows, co
                            attn::dec::SMEM_BYTES);
       attr = true;
     }
-    attn::dec::decode_tma_kernel<<<dim3(n_items, kv_heads, p.n_splits), attn::dec::NUM_THREADS,
-                                   attn::dec::SMEM_BYTES, st>>>(tk, tv, p);
+    launch_k(attn::dec::decode_tma_kernel, dim3(n_items, kv_heads, p.n_splits), attn::dec::NUM_THREADS, attn::dec::SMEM_BYTES, st, tk, tv, p);
     if (int rc = check_launch("attn_decode_tma_kernel")) return rc;
     if (p.n_splits > 1) {
-      attn::combine_kernel<<<dim3(n_items, q_heads), head_dim, 0, st>>>(p, head_dim);
+      launch_k(attn::combine_kernel, dim3(n_items, q_heads), head_dim, 0, st, p, head_dim);
       return check_launch("attn_combine_kernel");
     }
     return kOk;

@@ -94,6 +94,8 @@ __device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t smem_addr, uint32_t 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     prefill_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, const Params p) {
+  pdl_wait();  // inputs of this kernel are written by its predecessor
+  pdl_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -386,7 +388,7 @@ int launch_prefill_tc(const void* q, int64_t ldq, int64_t q_rows_total, const vo
     cudaFuncSetAttribute(prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr = true;
   }
-  prefill_tc_kernel<<<dim3(n_work, kv_heads), NUM_THREADS, SMEM_BYTES, st>>>(tq, tk, tv, p);
+  launch_k(prefill_tc_kernel, dim3(n_work, kv_heads), NUM_THREADS, SMEM_BYTES, st, tq, tk, tv, p);
   return check_launch("attn_prefill_tc_kernel");
 }
 

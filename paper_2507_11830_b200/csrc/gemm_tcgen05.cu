@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(NUM_THREADS, Tile<BN_>::MIN_BLOCKS)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  pdl_trigger();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -192,8 +193,13 @@ __global__ void __launch_bounds__(NUM_THREADS, Tile<BN_>::MIN_BLOCKS)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------------------------------------------- TMA producer
+      // PDL: the first ring of weight (B) tiles is fetched before pdl_wait();
+      // the activation (A) loads of those stages are issued after it.
       int stage = 0;
       uint32_t phase = 0;
+      int n_def = 0;
+      int def_stage[STAGES], def_kc[STAGES], def_m[STAGES], def_ko[STAGES];
+      bool waited = false;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
         int mb, nb, kb0, kb1, ks;
         split_coords(t, p, mb, nb, kb0, kb1, ks);
@@ -207,13 +213,33 @@ __global__ void __launch_bounds__(NUM_THREADS, Tile<BN_>::MIN_BLOCKS)
             ko = k / p.a_kchunk;
             kc = k - ko * p.a_kchunk;
           }
-          tma_load_3d(sa, &tmA, full + stage, kc, mb * BM, ko);
           tma_load_2d(sa + A_BYTES, &tmB, full + stage, k, nb * BN);
+          if (waited) {
+            tma_load_3d(sa, &tmA, full + stage, kc, mb * BM, ko);
+          } else {
+            def_stage[n_def] = stage;
+            def_kc[n_def] = kc;
+            def_m[n_def] = mb * BM;
+            def_ko[n_def] = ko;
+            if (++n_def == STAGES) {
+              pdl_wait();
+              waited = true;
+              for (int i = 0; i < n_def; ++i)
+                tma_load_3d(smem + def_stage[i] * STAGE_BYTES, &tmA, full + def_stage[i], def_kc[i],
+                            def_m[i], def_ko[i]);
+            }
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
+      }
+      if (!waited) {
+        pdl_wait();
+        for (int i = 0; i < n_def; ++i)
+          tma_load_3d(smem + def_stage[i] * STAGE_BYTES, &tmA, full + def_stage[i], def_kc[i],
+                      def_m[i], def_ko[i]);
       }
     }
     __syncwarp();
@@ -255,6 +281,7 @@ __global__ void __launch_bounds__(NUM_THREADS, Tile<BN_>::MIN_BLOCKS)
     __syncwarp();
   } else {
     // ----------------------------------------------------------- epilogue
+    pdl_wait();  // D (e.g. the residual stream) belongs to the predecessor until it completes
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     int acc = 0;
@@ -327,9 +354,214 @@ __global__ void __launch_bounds__(NUM_THREADS, Tile<BN_>::MIN_BLOCKS)
   }
 }
 
+// ------------------------------------------------------ swap-AB (decode-size M)
+// D^T = W · X^T: the 128-row MMA operand is a weight tile, the token rows (M <=
+// 128, padded to NT) are the N operand, so every staged byte is a weight byte.
+// Tiles = (128-row weight tile) x (K split); partials go to ws[split][M][N] and
+// splitk_reduce_kernel applies the epilogue, unless ksplit == 1 and the
+// epilogue is a plain store/add/GeLU (then it is applied here).
+template <int NT>
+struct SwapTile {
+  static constexpr int W_BYTES = 128 * BK * 2;
+  static constexpr int X_BYTES = NT * BK * 2;
+  static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
+  // M <= 32 (latency-bound decode): two CTAs per SM with ~100 KB rings, so a
+  // successor's CTAs can start streaming weights (PDL) while this one drains;
+  // larger M: one CTA per SM with a ~200 KB ring (measured best at B=64).
+  static constexpr int CTAS_PER_SM = NT <= 32 ? 2 : 1;
+  static constexpr int RING = (CTAS_PER_SM == 2 ? 100 : 200) * 1024;
+  static constexpr int STAGES = RING / STAGE_BYTES > 10 ? 10 : RING / STAGE_BYTES;
+  static constexpr int TMEM_COLS = 2 * NT < 32 ? 32 : 2 * NT;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NUM_THREADS, SwapTile<NT>::CTAS_PER_SM)
+    gemm_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                     const Params p) {
+  using T = SwapTile<NT>;
+  constexpr int STAGES = T::STAGES, STAGE_BYTES = T::STAGE_BYTES, TMEM_COLS = T::TMEM_COLS;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + ACC_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC_STAGES);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  pdl_trigger();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmW);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < ACC_STAGES; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int n_def = 0;
+      int def_stage[STAGES], def_kc[STAGES], def_ko[STAGES];
+      bool waited = false;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        const int ks = t % p.ksplit, nb = t / p.ksplit;
+        const int kb0 = ks * p.kb_per_split, kb1 = min(p.k_blocks, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          uint8_t* sw = smem + stage * STAGE_BYTES;
+          mbar_arrive_expect_tx(full + stage, STAGE_BYTES);
+          const int k = kb * BK;
+          int ko = 0, kc = k;
+          if (p.a_kchunk > 0) {
+            ko = k / p.a_kchunk;
+            kc = k - ko * p.a_kchunk;
+          }
+          tma_load_2d(sw, &tmW, full + stage, k, nb * 128);  // weights: no dependency
+          if (waited) {
+            tma_load_3d(sw + T::W_BYTES, &tmX, full + stage, kc, 0, ko);
+          } else {
+            def_stage[n_def] = stage;
+            def_kc[n_def] = kc;
+            def_ko[n_def] = ko;
+            if (++n_def == STAGES) {
+              pdl_wait();
+              waited = true;
+              for (int i = 0; i < n_def; ++i)
+                tma_load_3d(smem + def_stage[i] * STAGE_BYTES + T::W_BYTES, &tmX, full + def_stage[i],
+                            def_kc[i], 0, def_ko[i]);
+            }
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      if (!waited) {
+        pdl_wait();
+        for (int i = 0; i < n_def; ++i)
+          tma_load_3d(smem + def_stage[i] * STAGE_BYTES + T::W_BYTES, &tmX, full + def_stage[i],
+                      def_kc[i], 0, def_ko[i]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(128, NT);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        const int ks = t % p.ksplit;
+        const int kb0 = ks * p.kb_per_split, kb1 = min(p.k_blocks, kb0 + p.kb_per_split);
+        mbar_wait(tempty + acc, aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * NT;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(full + stage, phase);
+          tc_fence_after();
+          const uint32_t w_addr = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t x_addr = w_addr + T::W_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(d_tmem, sdesc_sw128(w_addr + k * 32), sdesc_sw128(x_addr + k * 32), idesc,
+                      (kb != kb0 || k != 0) ? 1u : 0u);
+          umma_commit(empty + stage);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(tfull + acc);
+        if (++acc == ACC_STAGES) {
+          acc = 0;
+          aphase ^= 1;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    pdl_wait();
+    const int quarter = warp & 3;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      const int ks = t % p.ksplit, nb = t / p.ksplit;
+      mbar_wait(tfull + acc, aphase);
+      tc_fence_after();
+      const int n = nb * 128 + quarter * 32 + lane;  // this thread's output feature
+      const uint32_t tb = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NT;
+#pragma unroll 1
+      for (int c = 0; c < NT; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tb + c, r);
+        tmem_ld_wait();
+        if (n < p.N) {
+          if (p.ws != nullptr) {
+            float* dst = p.ws + (int64_t)ks * p.M * p.N + n;
+#pragma unroll 4
+            for (int j = 0; j < 32; ++j)
+              if (c + j < p.M) dst[(int64_t)(c + j) * p.N] = __uint_as_float(r[j]);
+          } else {
+            int64_t col = n, base = 0;
+            if (p.peer_width > 0) {
+              const int64_t peer = n / p.peer_width;
+              col = n - peer * p.peer_width;
+              base = peer * p.peer_stride;
+            }
+#pragma unroll 4
+            for (int j = 0; j < 32; ++j) {
+              const int m = c + j;
+              if (m >= p.M) break;
+              float v = __uint_as_float(r[j]);
+              const int64_t off = base + (int64_t)m * p.ldd + col;
+              if (p.epi == SP_EPI_STORE_F32) {
+                reinterpret_cast<float*>(p.D)[off] = v;
+              } else if (p.epi == SP_EPI_ADD_F32) {
+                reinterpret_cast<float*>(p.D)[off] += v;
+              } else {
+                if (p.epi == SP_EPI_GELU) v = gelu_tanh(v);
+                reinterpret_cast<__nv_bfloat16*>(p.D)[off] = __float2bfloat16_rn(v);
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
+      if (++acc == ACC_STAGES) {
+        acc = 0;
+        aphase ^= 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
 // split-K reduction: v = sum_s ws[s] in ascending s (deterministic), then the
 // epilogue; one thread = 8 consecutive output columns of one row.
 __global__ void splitk_reduce_kernel(const Params p) {
+  pdl_wait();  // inputs of this kernel are written by its predecessor
+  pdl_trigger();
   const int n_out = p.epi == SP_EPI_SWIGLU ? p.N / 2 : p.N;
   const int64_t per_row = n_out / 8;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -521,14 +753,83 @@ static int launch(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_chunk_
     attr = true;
   }
   const int grid = std::min(p.num_tiles, sm_count() * T::MIN_BLOCKS);
-  gemm_kernel<BN><<<grid, NUM_THREADS, T::SMEM_BYTES, reinterpret_cast<cudaStream_t>(stream)>>>(
-      ta, tb, p);
+  launch_k(gemm_kernel<BN>, grid, NUM_THREADS, T::SMEM_BYTES, reinterpret_cast<cudaStream_t>(stream), ta, tb, p);
   if (int rc = check_launch("gemm_kernel")) return rc;
   if (ws) {
     const int n_out = epilogue == SP_EPI_SWIGLU ? N / 2 : N;
     const int64_t threads = (int64_t)M * (n_out / 8);
-    splitk_reduce_kernel<<<(unsigned)cdiv(threads, 256), 256, 0,
-                           reinterpret_cast<cudaStream_t>(stream)>>>(p);
+    launch_k(splitk_reduce_kernel, (unsigned)cdiv(threads, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream), p);
+    return check_launch("splitk_reduce_kernel");
+  }
+  return kOk;
+}
+
+template <int NT>
+static int launch_swap(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_chunk_stride,
+                       const void* B, int64_t ldb, void* D, int64_t ldd, int M, int N, int K,
+                       int epilogue, int64_t peer_width, int64_t peer_stride, void* stream,
+                       float* ws, int64_t ws_bytes) {
+  using namespace sp::gemm;
+  using T = SwapTile<NT>;
+  const int sms = sm_count();
+  const int64_t k_blocks = cdiv(K, BK);
+  const int64_t n_tiles = cdiv(N, 128);
+  // split K so the tile count is close to the resident-CTA count
+  const int64_t slots = (int64_t)sms * T::CTAS_PER_SM;
+  int64_t ks = std::max<int64_t>(1, (slots + n_tiles / 2) / n_tiles);
+  ks = std::min<int64_t>(ks, std::max<int64_t>(1, k_blocks / 2));
+  const int64_t per = cdiv(k_blocks, ks);
+  ks = cdiv(k_blocks, per);
+  const bool direct = ks == 1 && epilogue != SP_EPI_SWIGLU;
+  if (!direct && (!ws || ks * (int64_t)M * N * 4 > ws_bytes)) return -1;  // caller falls back
+  CUtensorMap tx, tw;
+  {
+    const uint64_t kin = a_kchunk > 0 ? (uint64_t)a_kchunk : (uint64_t)K;
+    const uint64_t kout = a_kchunk > 0 ? (uint64_t)(K / a_kchunk) : 1;
+    const uint64_t cstride = a_kchunk > 0 ? (uint64_t)a_chunk_stride * 2
+                                          : (uint64_t)lda * 2 * (uint64_t)M;
+    uint64_t dims[3] = {kin, (uint64_t)M, kout};
+    uint64_t strides[2] = {(uint64_t)lda * 2, cstride};
+    uint32_t box[3] = {BK, (uint32_t)NT, 1};
+    if (int rc = get_map(&tx, A, 3, dims, strides, box)) return rc;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)K, (uint64_t)N};
+    uint64_t strides[1] = {(uint64_t)ldb * 2};
+    uint32_t box[2] = {BK, 128};
+    if (int rc = get_map(&tw, B, 2, dims, strides, box)) return rc;
+  }
+  Params p;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.num_m = 1;
+  p.num_n = (int)n_tiles;
+  p.k_blocks = (int)k_blocks;
+  p.epi = epilogue;
+  p.a_kchunk = (int)(a_kchunk > 0 ? a_kchunk : 0);
+  p.D = D;
+  p.ldd = ldd;
+  p.peer_width = peer_width;
+  p.peer_stride = peer_stride;
+  p.group_m = 1;
+  p.ws = direct ? nullptr : ws;
+  p.ksplit = (int)ks;
+  p.kb_per_split = (int)per;
+  p.num_tiles = (int)(n_tiles * ks);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_swap_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         T::SMEM_BYTES);
+    attr = true;
+  }
+  const int grid = (int)std::min<int64_t>(p.num_tiles, slots);
+  launch_k(gemm_swap_kernel<NT>, grid, NUM_THREADS, T::SMEM_BYTES, reinterpret_cast<cudaStream_t>(stream), tx, tw, p);
+  if (int rc = check_launch("gemm_swap_kernel")) return rc;
+  if (!direct) {
+    const int n_out = epilogue == SP_EPI_SWIGLU ? N / 2 : N;
+    const int64_t threads = (int64_t)M * (n_out / 8);
+    launch_k(splitk_reduce_kernel, (unsigned)cdiv(threads, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream), p);
     return check_launch("splitk_reduce_kernel");
   }
   return kOk;
@@ -580,15 +881,19 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
   const bool no_split = getenv("SP_GEMM_NO_SPLITK") != nullptr;
   int bn = 256;
   if (m_tiles * cdiv(N, 256) < sms) {
-    if (m_tiles == 1 && g_ws && !no_split && N % 32 == 0 && k_blocks >= 4) {
-      const int64_t base = cdiv(N, 64);
-      int64_t ks = (2 * sms) / base;
-      ks = std::max<int64_t>(1, std::min<int64_t>(ks, k_blocks / 4));
-      const int64_t per = cdiv(k_blocks, ks);
-      ks = cdiv(k_blocks, per);
-      if (ks * (int64_t)M * N * 4 <= g_ws_bytes && (ks > 1 || epilogue == SP_EPI_SWIGLU))
-        return launch<64>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
-                          peer_width, peer_stride, stream, g_ws, (int)ks);
+    if (m_tiles == 1 && !no_split && N % 32 == 0) {
+      // decode-size M: swap-AB weight streaming (+ split-K / fused epilogue)
+      int rc = -1;
+      if (M <= 32)
+        rc = launch_swap<32>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
+                             peer_width, peer_stride, stream, g_ws, g_ws_bytes);
+      else if (M <= 64)
+        rc = launch_swap<64>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
+                             peer_width, peer_stride, stream, g_ws, g_ws_bytes);
+      else
+        rc = launch_swap<128>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
+                              peer_width, peer_stride, stream, g_ws, g_ws_bytes);
+      if (rc >= 0) return rc;
     }
     if (epilogue != SP_EPI_SWIGLU) {
       bn = 32;

@@ -3,6 +3,7 @@
 // all-to-all pack/unpack, loopback add, argmax and row gather.
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/shiftpar.h"
@@ -21,6 +22,15 @@ int fail(int code, const std::string& msg) {
 
 static std::atomic<long long> g_launches{0};
 
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SP_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 int check_launch(const char* what) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
@@ -32,6 +42,8 @@ int check_launch(const char* what) {
 __global__ void embed_kernel(const int32_t* __restrict__ ids, const __nv_bfloat16* __restrict__ table,
                              const int32_t* __restrict__ pos, const float* __restrict__ pos_table,
                              float* __restrict__ out, int hidden) {
+  pdl_wait();  // inputs of this kernel are written by its predecessor
+  pdl_trigger();
   const int r = blockIdx.x;
   const int64_t tok = ids[r];
   const __nv_bfloat16* src = table + tok * hidden;
@@ -57,6 +69,8 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, int64_t ldx, const flo
                                    const float* __restrict__ gain, float eps,
                                    const int32_t* __restrict__ row_idx,
                                    __nv_bfloat16* __restrict__ out, int64_t ldo, int hidden) {
+  pdl_wait();  // inputs of this kernel are written by its predecessor
+  pdl_trigger();
   const int r = blockIdx.x;
   const int64_t src_row = row_idx ? row_idx[r] : r;
   float* xr = x + src_row * ldx;
@@ -112,21 +126,26 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, int64_t ldx, const flo
 }
 
 // ------------------------------------------------- RoPE + paged KV write
-// one warp per (token, head); lanes cover the d/2 rotation pairs
+// 8 threads per (token, head): thread j owns rotation pairs [8j, 8j+8) of a
+// 128-dim head (16-byte loads of both halves, one float4x2 of cos/sin each);
+// generic head_dim falls back to one pair per lane.
 __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldqkv,
                                const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,
                                const float* __restrict__ rope, __nv_bfloat16* __restrict__ q_out,
                                int64_t ldq, __nv_bfloat16* __restrict__ k_pool,
                                __nv_bfloat16* __restrict__ v_pool, int rows, int q_heads,
                                int kv_heads, int head_dim, int block_size) {
+  pdl_wait();  // inputs of this kernel are written by its predecessor
+  pdl_trigger();
   const int heads = q_heads + 2 * kv_heads;
-  const int warps_per_block = blockDim.x >> 5;
-  const int64_t item = (int64_t)blockIdx.x * warps_per_block + (threadIdx.x >> 5);
+  const int half = head_dim >> 1;
+  const int tpg = half / 8;  // threads per (token, head) when vectorised
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t item = gid / tpg;
   if (item >= (int64_t)rows * heads) return;
+  const int j = (int)(gid % tpg);
   const int r = (int)(item / heads);
   const int h = (int)(item % heads);
-  const int lane = threadIdx.x & 31;
-  const int half = head_dim >> 1;
   const __nv_bfloat16* src = qkv + (int64_t)r * ldqkv + (int64_t)h * head_dim;
   __nv_bfloat16* dst;
   if (h < q_heads) {
@@ -141,25 +160,33 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld
     dst = pool + ((blk * kv_heads + kvh) * block_size + off) * head_dim;
   }
   const bool rotate = rope != nullptr && h < q_heads + kv_heads;
-  const float* cs = rotate ? rope + (int64_t)pos[r] * half * 2 : nullptr;
-  for (int i = lane; i < half; i += 32) {
-    float a = __bfloat162float(src[i]);
-    float b = __bfloat162float(src[i + half]);
-    if (rotate) {
-      const float c = cs[2 * i], s = cs[2 * i + 1];
-      const float na = a * c - b * s;
-      const float nb = b * c + a * s;
-      a = na;
-      b = nb;
+  const int i0 = j * 8;
+  uint4 ua = *reinterpret_cast<const uint4*>(src + i0);
+  uint4 ub = *reinterpret_cast<const uint4*>(src + half + i0);
+  if (rotate) {
+    const float4* cs = reinterpret_cast<const float4*>(rope + ((int64_t)pos[r] * half + i0) * 2);
+    uint32_t* pa = reinterpret_cast<uint32_t*>(&ua);
+    uint32_t* pb = reinterpret_cast<uint32_t*>(&ub);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 c2 = cs[q];  // (cos, sin) of pairs i0+2q and i0+2q+1
+      const float2 a = unpack_bf16x2(pa[q]);
+      const float2 b = unpack_bf16x2(pb[q]);
+      const float na0 = a.x * c2.x - b.x * c2.y, nb0 = b.x * c2.x + a.x * c2.y;
+      const float na1 = a.y * c2.z - b.y * c2.w, nb1 = b.y * c2.z + a.y * c2.w;
+      pa[q] = pack_bf16x2(na0, na1);
+      pb[q] = pack_bf16x2(nb0, nb1);
     }
-    dst[i] = __float2bfloat16_rn(a);
-    dst[i + half] = __float2bfloat16_rn(b);
   }
+  *reinterpret_cast<uint4*>(dst + i0) = ua;
+  *reinterpret_cast<uint4*>(dst + half + i0) = ub;
 }
 
 // ------------------------------------------------------ a2a pack/unpack
 __global__ void pack_kernel(const uint4* __restrict__ src, int64_t lds_v, uint4* __restrict__ dst,
                             int rows, int peers, int width_v) {
+  pdl_wait();  // inputs of this kernel are written by its predecessor
+  pdl_trigger();
   const int64_t total = (int64_t)rows * peers * width_v;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -172,6 +199,8 @@ __global__ void pack_kernel(const uint4* __restrict__ src, int64_t lds_v, uint4*
 
 __global__ void unpack_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int64_t ldd_v,
                               int rows, int peers, int width_v) {
+  pdl_wait();  // inputs of this kernel are written by its predecessor
+  pdl_trigger();
   const int64_t total = (int64_t)rows * peers * width_v;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -185,6 +214,8 @@ __global__ void unpack_kernel(const uint4* __restrict__ src, uint4* __restrict__
 // ------------------------------------------------------------ small ops
 __global__ void add_f32_kernel(const float4* __restrict__ a, const float4* __restrict__ b,
                                float4* __restrict__ d, int64_t n4) {
+  pdl_wait();  // inputs of this kernel are written by its predecessor
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
     float4 x = a[i], y = b[i];
@@ -193,12 +224,16 @@ __global__ void add_f32_kernel(const float4* __restrict__ a, const float4* __res
 }
 
 __global__ void add_f32_tail_kernel(const float* a, const float* b, float* d, int64_t lo, int64_t n) {
+  pdl_wait();  // inputs of this kernel are written by its predecessor
+  pdl_trigger();
   int64_t i = lo + threadIdx.x;
   if (i < n) d[i] = a[i] + b[i];
 }
 
 __global__ void argmax_kernel(const float* __restrict__ logits, int64_t ld, int vocab,
                               int32_t* __restrict__ idx, float* __restrict__ val) {
+  pdl_wait();  // inputs of this kernel are written by its predecessor
+  pdl_trigger();
   const float* row = logits + (int64_t)blockIdx.x * ld;
   float best = -INFINITY;
   int bi = 0x7fffffff;
@@ -248,6 +283,8 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int64_t ld, int 
 __global__ void gather_rows_kernel(const float* __restrict__ src, int64_t lds,
                                    const int32_t* __restrict__ idx, float* __restrict__ dst,
                                    int64_t ldd, int width) {
+  pdl_wait();  // inputs of this kernel are written by its predecessor
+  pdl_trigger();
   const float* s = src + (int64_t)idx[blockIdx.x] * lds;
   float* d = dst + (int64_t)blockIdx.x * ldd;
   for (int c = threadIdx.x; c < width; c += blockDim.x) d[c] = s[c];
@@ -292,7 +329,7 @@ extern "C" sp_status sp_embed(const int32_t* ids, const void* table_bf16, const 
   if (rows < 0 || hidden <= 0 || hidden % 8) return fail(kInvalid, "embed: hidden % 8 != 0");
   if (rows == 0) return kOk;
   if (pos_table && !pos) return fail(kInvalid, "embed: pos_table without positions");
-  embed_kernel<<<rows, 128, 0, S(stream)>>>(ids, static_cast<const __nv_bfloat16*>(table_bf16), pos,
+  launch_k(embed_kernel, rows, 128, 0, S(stream), ids, static_cast<const __nv_bfloat16*>(table_bf16), pos,
                                             pos_table, out_f32, hidden);
   return check_launch("embed_kernel");
 }
@@ -308,12 +345,12 @@ extern "C" sp_status sp_add_rmsnorm(float* x, int64_t ldx, const float* add, con
   const int per = (hidden + threads * 4 - 1) / (threads * 4);
   auto out = static_cast<__nv_bfloat16*>(out_bf16);
   switch (per) {
-    case 1: add_rmsnorm_kernel<1><<<rows, threads, 0, S(stream)>>>(x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
-    case 2: add_rmsnorm_kernel<2><<<rows, threads, 0, S(stream)>>>(x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
-    case 3: add_rmsnorm_kernel<3><<<rows, threads, 0, S(stream)>>>(x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
-    case 4: add_rmsnorm_kernel<4><<<rows, threads, 0, S(stream)>>>(x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
+    case 1: launch_k(add_rmsnorm_kernel<1>, rows, threads, 0, S(stream), x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
+    case 2: launch_k(add_rmsnorm_kernel<2>, rows, threads, 0, S(stream), x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
+    case 3: launch_k(add_rmsnorm_kernel<3>, rows, threads, 0, S(stream), x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
+    case 4: launch_k(add_rmsnorm_kernel<4>, rows, threads, 0, S(stream), x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
     case 5: case 6: case 7: case 8:
-      add_rmsnorm_kernel<8><<<rows, threads, 0, S(stream)>>>(x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
+      launch_k(add_rmsnorm_kernel<8>, rows, threads, 0, S(stream), x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
     default: return fail(kUnsupported, "add_rmsnorm: hidden > 8192");
   }
   return check_launch("add_rmsnorm_kernel");
@@ -328,13 +365,14 @@ extern "C" sp_status sp_rope_kv_write(const void* qkv, int64_t ldqkv, const int3
     return fail(kInvalid, "rope_kv_write: bad geometry");
   if (rows == 0 || q_heads + kv_heads == 0) return kOk;
   if (kv_heads > 0 && (!k_pool || !v_pool || !slot)) return fail(kInvalid, "rope_kv_write: null pool/slot");
+  if (head_dim % 16) return fail(kUnsupported, "rope_kv_write: head_dim must be a multiple of 16");
+  if (ldqkv % 8 || (q_out && ldq % 8)) return fail(kInvalid, "rope_kv_write: rows must be 16-byte aligned");
   const int heads = q_heads + 2 * kv_heads;
-  const int64_t warps = (int64_t)rows * heads;
-  const int wpb = 8;
-  rope_kv_kernel<<<(unsigned)((warps + wpb - 1) / wpb), wpb * 32, 0, S(stream)>>>(
-      static_cast<const __nv_bfloat16*>(qkv), ldqkv, pos, slot, rope_table,
-      static_cast<__nv_bfloat16*>(q_out), ldq, static_cast<__nv_bfloat16*>(k_pool),
-      static_cast<__nv_bfloat16*>(v_pool), rows, q_heads, kv_heads, head_dim, block_size);
+  const int64_t threads = (int64_t)rows * heads * (head_dim / 16);
+  launch_k(rope_kv_kernel, (unsigned)((threads + 255) / 256), 256, 0, S(stream),
+           static_cast<const __nv_bfloat16*>(qkv), ldqkv, pos, slot, rope_table,
+           static_cast<__nv_bfloat16*>(q_out), ldq, static_cast<__nv_bfloat16*>(k_pool),
+           static_cast<__nv_bfloat16*>(v_pool), rows, q_heads, kv_heads, head_dim, block_size);
   return check_launch("rope_kv_kernel");
 }
 
@@ -344,7 +382,7 @@ extern "C" sp_status sp_a2a_pack(const void* src, int64_t lds, void* dst, int ro
     return fail(kInvalid, "a2a_pack: width and stride must be multiples of 8");
   if (rows == 0) return kOk;
   const int64_t n = (int64_t)rows * peers * (width / 8);
-  pack_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(static_cast<const uint4*>(src), lds / 8,
+  launch_k(pack_kernel, grid_for(n, 256), 256, 0, S(stream), static_cast<const uint4*>(src), lds / 8,
                                                       static_cast<uint4*>(dst), rows, peers, width / 8);
   return check_launch("pack_kernel");
 }
@@ -355,7 +393,7 @@ extern "C" sp_status sp_a2a_unpack(const void* src, void* dst, int64_t ldd, int 
     return fail(kInvalid, "a2a_unpack: width and stride must be multiples of 8");
   if (rows == 0) return kOk;
   const int64_t n = (int64_t)rows * peers * (width / 8);
-  unpack_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(static_cast<const uint4*>(src),
+  launch_k(unpack_kernel, grid_for(n, 256), 256, 0, S(stream), static_cast<const uint4*>(src),
                                                         static_cast<uint4*>(dst), ldd / 8, rows,
                                                         peers, width / 8);
   return check_launch("unpack_kernel");
@@ -368,10 +406,9 @@ extern "C" sp_status sp_add_f32(const float* a, const float* b, float* dst, int6
        reinterpret_cast<uintptr_t>(dst)) & 15)
     return fail(kInvalid, "add_f32: pointers must be 16-byte aligned");
   const int64_t n4 = n / 4;
-  if (n4) add_f32_kernel<<<grid_for(n4, 256), 256, 0, S(stream)>>>(
-      reinterpret_cast<const float4*>(a), reinterpret_cast<const float4*>(b),
+  if (n4) launch_k(add_f32_kernel, grid_for(n4, 256), 256, 0, S(stream), reinterpret_cast<const float4*>(a), reinterpret_cast<const float4*>(b),
       reinterpret_cast<float4*>(dst), n4);
-  if (n % 4) add_f32_tail_kernel<<<1, 32, 0, S(stream)>>>(a, b, dst, n4 * 4, n);
+  if (n % 4) launch_k(add_f32_tail_kernel, 1, 32, 0, S(stream), a, b, dst, n4 * 4, n);
   return check_launch("add_f32_kernel");
 }
 
@@ -379,7 +416,7 @@ extern "C" sp_status sp_argmax(const float* logits, int64_t ld, int rows, int vo
                                float* val, void* stream) {
   if (rows < 0 || vocab <= 0) return fail(kInvalid, "argmax: bad shape");
   if (rows == 0) return kOk;
-  argmax_kernel<<<rows, 1024, 0, S(stream)>>>(logits, ld, vocab, idx, val);
+  launch_k(argmax_kernel, rows, 1024, 0, S(stream), logits, ld, vocab, idx, val);
   return check_launch("argmax_kernel");
 }
 
@@ -387,6 +424,6 @@ extern "C" sp_status sp_gather_rows_f32(const float* src, int64_t lds, const int
                                         int64_t ldd, int rows, int width, void* stream) {
   if (rows < 0 || width <= 0) return fail(kInvalid, "gather_rows: bad shape");
   if (rows == 0) return kOk;
-  gather_rows_kernel<<<rows, 256, 0, S(stream)>>>(src, lds, idx, dst, ldd, width);
+  launch_k(gather_rows_kernel, rows, 256, 0, S(stream), src, lds, idx, dst, ldd, width);
   return check_launch("gather_rows_kernel");
 }

@@ -40,7 +40,7 @@ from . import ops
 from .config import ModelConfig
 from .errors import CacheOverflow, ConfigError, ContractViolation
 from .fabric import CommRecord, DeviceGroup, LoopbackGroup
-from .flops import FlopMeter, PassShape, shard_bounds, shard_rows
+from .flops import FlopMeter, PassShape, flop_count, shard_bounds, shard_rows
 from .kv_cache import KvCache, KvPool
 from .weights import ModelWeights
 
@@ -192,10 +192,21 @@ class _Meta:
     pass
 
 
+class _GraphEntry:
+    """A captured decode pass: static metadata buffer, graph, static outputs."""
+
+    def __init__(self):
+        self.dev: Optional[torch.Tensor] = None
+        self.graph = None
+        self.outputs: List[torch.Tensor] = []
+        self.charges: list = []
+        self.kernels = 0
+
+
 class Engine:
     def __init__(self, weights: ModelWeights, group: DeviceGroup, policy: ShiftPolicy,
                  swiftkv: Optional[SwiftKvConfig] = None, *, num_blocks: Optional[int] = None,
-                 block_size: int = 64):
+                 block_size: int = 64, cuda_graphs: bool = True):
         cfg = weights.config
         self.weights = weights
         self.config: ModelConfig = cfg
@@ -229,7 +240,12 @@ class Engine:
         self._pinned: List[torch.Tensor] = []
         self._pin_events: List[Optional[torch.cuda.Event]] = []
         self._pin_idx = 0
-        self._ws: Optional[torch.Tensor] = None
+        # attention split-KV workspace, allocated once (graph replays need static buffers)
+        self._ws = torch.empty(16 << 20, dtype=torch.float32, device=self.device)
+        self.cuda_graphs = cuda_graphs
+        self._graphs: Dict[tuple, _GraphEntry] = {}
+        self._graph_pool = torch.cuda.graph_pool_handle() if cuda_graphs else None
+        self._capturing = False
 
     # ---------------------------------------------------------- sequences
     def new_sequence(self, seq_id: int, capacity: Optional[int] = None) -> Sequence:
@@ -277,15 +293,34 @@ class Engine:
                                 f"{alloc.free_blocks} free")
         for it in batch.items:
             alloc.reserve(it.seq.cache.key, it.seq.cache.token_count + len(it.tokens))
-        meta = self._metadata(batch, mode, span_logits, cut_full if use_swiftkv else None)
+        cut = cut_full if use_swiftkv else None
+        graph_key = None
+        if (self.cuda_graphs and cut is None and not span_logits
+                and all(len(it.tokens) == 1 for it in batch.items)):
+            graph_key = (mode, len(batch.items), self._bt_width_cap(batch))
+        shape = self.pass_shape(batch, span_logits) if graph_key else None
+        meta = self._metadata(batch, mode, span_logits, cut, graph_key=graph_key)
         self.group.begin_step(self._step_counter)
         rec_start = len(self.group.records)
         meters = [FlopMeter() for _ in range(self.world_size)]
-        cut = cut_full if use_swiftkv else None
-        if mode is ParallelMode.TP:
-            logits = self._forward_tp(meta, batch, meters, span_logits, cut)
+        entry = self._graphs.get(graph_key) if graph_key else None
+        if entry is not None and entry.graph is not None:
+            # replay: host bookkeeping + ledger exactly as the eager pass would record
+            for layer in range(self.config.n_layers):
+                self._stage_all(layer, batch)
+            for kind, per_dev in entry.charges:
+                self.group.charge(kind, per_dev)
+            entry.graph.replay()
+            ops.add_graph_launches(entry.kernels)
+            logits = [t.clone() for t in entry.outputs]
+            flops = flop_count(shape, mode, self.config, self.world_size)
+            for m, f in zip(meters, flops):
+                m.flops = f
         else:
-            logits = self._forward_sp(meta, batch, meters, span_logits, cut)
+            fwd = self._forward_tp if mode is ParallelMode.TP else self._forward_sp
+            logits = fwd(meta, batch, meters, span_logits, cut)
+            if graph_key is not None:
+                self._capture(graph_key, meta, batch, fwd)
         for it in batch.items:
             it.seq.cache.commit(len(it.tokens))
         record = StepRecord(step_id=self._step_counter, mode=mode, kind=batch.kind,
@@ -297,6 +332,39 @@ class Engine:
         self.step_records.append(record)
         self._step_counter += 1
         return logits, record
+
+    def _bt_width_cap(self, batch: Batch) -> int:
+        """Block-table width for graph keys: covers every item's capacity,
+        rounded up to a power of two so the key is stable while sequences grow."""
+        bs = self.pool.block_size
+        need = max(-(-it.seq.cache.capacity // bs) for it in batch.items)
+        w = 1
+        while w < need:
+            w *= 2
+        return w
+
+    def _capture(self, key, meta: "_Meta", batch: Batch, fwd) -> None:
+        """Record the decode pass just executed eagerly as a CUDA graph (same
+        static metadata buffer); later passes with the same key replay it."""
+        entry = self._graphs[key]
+        n_rec = len(self.group.records)
+        k0 = ops.kernel_launches()
+        graph = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        self._capturing = True
+        try:
+            with torch.cuda.graph(graph, pool=self._graph_pool):
+                outs = fwd(meta, batch, [FlopMeter() for _ in range(self.world_size)], False, None)
+        finally:
+            self._capturing = False
+        entry.kernels = ops.kernel_launches() - k0
+        events = {}
+        for r in self.group.records[n_rec:]:
+            events.setdefault(r.event_id, [r.kind, [0.0] * self.world_size])[1][r.device] = r.bytes
+        entry.charges = [tuple(events[e]) for e in sorted(events)]
+        del self.group.records[n_rec:]
+        entry.outputs = outs
+        entry.graph = graph
 
     def forward_tp(self, batch: Batch, span_logits: bool = False):
         return self.step(batch, mode=ParallelMode.TP, span_logits=span_logits)
@@ -334,7 +402,7 @@ class Engine:
         return self._pinned[i], i
 
     def _metadata(self, batch: Batch, mode: ParallelMode, span_logits: bool,
-                  cut: Optional[int]) -> _Meta:
+                  cut: Optional[int], graph_key=None) -> _Meta:
         """Flatten the batch (parallel_engine.py:307-329) and build every index
         array the kernels need; one pinned H2D copy."""
         cfg = self.config
@@ -355,6 +423,8 @@ class Engine:
         first = np.asarray(hist, dtype=np.int32)
         kvlen = first + np.asarray(spans, dtype=np.int32)
         width = max(len(alloc.tables[it.seq.cache.key]) for it in items)
+        if graph_key is not None:
+            width = graph_key[2]
         bt = np.zeros((n, width), dtype=np.int32)
         for i, it in enumerate(items):
             tab = alloc.tables[it.seq.cache.key]
@@ -387,7 +457,13 @@ class Engine:
         # every array starts on a 16-byte boundary (the kernels read int2 pairs)
         total = sum(-(-a.size // 4) * 4 for a in parts.values())
         host, idx = self._pinned_buffer(total)
-        dev = torch.empty(max(total, 1), dtype=torch.int32, device=self.device)
+        if graph_key is not None:
+            entry = self._graphs.setdefault(graph_key, _GraphEntry())
+            if entry.dev is None:
+                entry.dev = torch.empty(max(total, 1), dtype=torch.int32, device=self.device)
+            dev = entry.dev
+        else:
+            dev = torch.empty(max(total, 1), dtype=torch.int32, device=self.device)
         views = {}
         off = 0
         hv = host.numpy()
@@ -420,9 +496,7 @@ class Engine:
         return meta
 
     def _workspace(self, n_items: int, q_heads: int, max_kv: int) -> Optional[torch.Tensor]:
-        need = ops.attn_workspace_bytes(n_items, q_heads, self.config.head_dim, max_kv)
-        if self._ws is None or self._ws.numel() * 4 < need:
-            self._ws = torch.empty((need + 3) // 4, dtype=torch.float32, device=self.device)
+        # fixed 64 MB: the kernel falls back to one split when a pass would need more
         return self._ws
 
     # ------------------------------------------------------- shared pieces
@@ -471,6 +545,8 @@ class Engine:
 
     def _stage_all(self, layer: int, batch: Batch) -> None:
         # every process tracks the global cursors: all P devices append this layer
+        if self._capturing:
+            return  # graph capture re-records a pass whose writes are already counted
         for it in batch.items:
             for dev in range(self.world_size):
                 it.seq.cache._stage(dev, layer, len(it.tokens))

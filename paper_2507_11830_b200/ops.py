@@ -40,21 +40,32 @@ class _Timed:
         self.kind, self.flops, self.nbytes = kind, flops, nbytes
 
     def __enter__(self):
-        if PROFILE is not None:
+        self.on = PROFILE is not None and not torch.cuda.is_current_stream_capturing()
+        if self.on:
             self.ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             self.ev[0].record()
         return self
 
     def __exit__(self, *exc):
-        if PROFILE is not None and exc[0] is None:
+        if self.on and exc[0] is None:
             self.ev[1].record()
             PROFILE.setdefault(self.kind, []).append((self.ev[0], self.ev[1], self.flops, self.nbytes))
         return False
 
 
+_graph_launches = 0
+
+
+def add_graph_launches(n: int) -> None:
+    """Account kernels launched by a CUDA-graph replay (not seen by the C counter)."""
+    global _graph_launches
+    _graph_launches += n
+
+
 def kernel_launches() -> int:
-    """Kernels libshiftpar.so has launched in this process (counted in C)."""
-    return int(_lib.load().sp_kernel_launches())
+    """Kernels of libshiftpar.so launched in this process: counted in C for direct
+    launches, plus the kernel nodes of every replayed CUDA graph."""
+    return int(_lib.load().sp_kernel_launches()) + _graph_launches
 
 
 def _stream() -> int:

@@ -366,3 +366,33 @@ def test_head_dim_128_tcgen05_attention_matches_oracle(d128, mode):
             h.append(t)
             want, _ = oracle.forward_reference(d128, h)
             assert rel_err(got.cpu().numpy(), want[-1]) <= LOGIT_TOL
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_cuda_graph_decode_matches_eager(c1, p):
+    """Decode passes replayed from CUDA graphs give bit-identical logits, the
+    same cache bookkeeping and the same comm ledger as eager passes."""
+    prompts = [c1_prompts()[i][:n] for i, n in ((0, 40), (1, 25), (2, 33))]
+    res = {}
+    for graphs in (False, True):
+        eng = Engine(device_weights(c1, p), LoopbackGroup(p), ShiftPolicy(token_threshold=3),
+                     cuda_graphs=graphs)
+        seqs = [eng.new_sequence(i, capacity=80) for i in range(3)]
+        eng.step(Batch(BatchKind.PREFILL, [BatchItem(s, q) for s, q in zip(seqs, prompts)]))
+        outs, recs = [], []
+        toks = [1, 2, 3]
+        for step in range(6):
+            sub = seqs if step % 3 != 2 else seqs[:2]  # batch 3 -> SP, batch 2 -> TP (tau=3)
+            lg, rec = eng.step(Batch(BatchKind.DECODE, [BatchItem(s, [t]) for s, t in zip(sub, toks)]))
+            outs.append([x.cpu() for x in lg])
+            recs.append((rec.mode, rec.flops_per_device, rec.comm))
+            toks = [int(torch.argmax(x)) for x in lg] + [5]
+        res[graphs] = (outs, recs, [s.cache.write_counter for s in seqs],
+                       [s.cache.token_count for s in seqs])
+        if graphs:
+            assert len(eng._graphs) >= 2  # SP and TP keys captured
+    (o0, r0, w0, t0), (o1, r1, w1, t1) = res[False], res[True]
+    assert r0 == r1 and w0 == w1 and t0 == t1
+    for a, b in zip(o0, o1):
+        for x, y in zip(a, b):
+            assert torch.equal(x, y)

@@ -331,14 +331,15 @@ def test_gemm_tile_width_variants_are_bitexact(monkeypatch):
     assert rel(outs["32"][0], a.float() @ b.float().t()) < 1e-4
 
 
-@pytest.mark.parametrize("epi", ["f32", "add", "bf16", "swiglu", "gelu", "peer"])
-def test_gemm_split_k_regime(epi):
+@pytest.mark.parametrize("M", [1, 48, 100])
+@pytest.mark.parametrize("epi", ["f32", "add", "bf16", "swiglu", "gelu", "peer", "chunked"])
+def test_gemm_split_k_regime(epi, M):
     """Decode-size M: split-K over BN=64 tiles with an ascending-order reduce.
     Deterministic run to run; within f32 accumulation noise of the reference."""
     ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
     ops.set_gemm_workspace(ws)
     try:
-        M, N, K = 48, 1024, 4096
+        N, K = 1024, 4096
         a, b = rnd(M, K, seed=40), rnd(N, K, seed=41)
         ref = a.float() @ b.float().t()
         outs = []
@@ -366,6 +367,13 @@ def test_gemm_split_k_regime(epi):
                 v = ref.view(M, f // 128, 2, 128)
                 want = (torch.nn.functional.silu(v[:, :, 0]) * v[:, :, 1]).reshape(M, f)
                 tol = 1e-2
+            elif epi == "chunked":
+                P, w = 4, K // 4  # SP O-proj: A is the [P][rows][w] all-to-all receive
+                back = torch.cat([a[:, s * w:(s + 1) * w] for s in range(P)], dim=0).contiguous()
+                d = torch.zeros(M, N, device="cuda")
+                ops.gemm(back, b, d, ops.EPI_ADD_F32, M=M, N=N, K=K, lda=w, ldb=K, ldd=N,
+                         a_kchunk=w, a_chunk_stride=M * w)
+                want, tol = ref, 1e-4
             else:
                 P, W = 4, N // 4
                 d = torch.empty(P * M, W, device="cuda", dtype=torch.bfloat16)
