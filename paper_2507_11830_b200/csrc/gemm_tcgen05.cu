@@ -557,6 +557,256 @@ __global__ void __launch_bounds__(NUM_THREADS, SwapTile<NT>::CTAS_PER_SM)
   }
 }
 
+// ------------------------------------------------ 2-CTA (cta_group::2) kernel
+// A CTA pair on one TPC computes a 256x256 tile: CTA r holds A rows
+// [m0 + 128 r, +128) and B rows [n0 + 128 r, +128) in its own shared memory;
+// the leader (rank 0) issues tcgen05.mma.cta_group::2 M=256 N=256, which reads
+// both CTAs' operands and writes each CTA's 128 accumulator rows into its own
+// TMEM.  Per SM this halves the B bytes staged per FLOP vs the 1-CTA kernel.
+namespace pair {
+constexpr int STAGES = 6;
+constexpr int A_BYTES = 128 * BK * 2;
+constexpr int B_BYTES = 128 * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// TMA whose completion bytes land on the LEADER's barrier (peer bit cleared)
+__device__ __forceinline__ void tma2_load_2d(void* dst, const void* desc, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(desc), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma2_load_3d(void* dst, const void* desc, uint64_t* bar, int c0, int c1,
+                                             int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(desc), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void umma2_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+}  // namespace pair
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + pair::STAGES * pair::STAGE_BYTES);
+  uint64_t* empty = full + pair::STAGES;
+  uint64_t* tfull = empty + pair::STAGES;
+  uint64_t* tempty = tfull + ACC_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC_STAGES);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = pair::cta_rank();
+  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+  pdl_trigger();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < pair::STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < ACC_STAGES; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 8);  // 4 epilogue warps x 2 CTAs (leader's barrier is used)
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  pair::cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int n_def = 0;
+      int def_stage[pair::STAGES], def_kc[pair::STAGES], def_m[pair::STAGES], def_ko[pair::STAGES];
+      bool waited = false;
+      for (int t = cluster; t < p.num_tiles; t += n_clusters) {
+        int mb, nb;
+        tile_coords(t, p, mb, nb);
+        const int m0 = mb * 256 + rank * 128;
+        const int n0 = nb * 256 + rank * 128;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          uint8_t* sa = smem + stage * pair::STAGE_BYTES;
+          if (rank == 0) mbar_arrive_expect_tx(full + stage, 2 * pair::STAGE_BYTES);
+          const int k = kb * BK;
+          int ko = 0, kc = k;
+          if (p.a_kchunk > 0) {
+            ko = k / p.a_kchunk;
+            kc = k - ko * p.a_kchunk;
+          }
+          pair::tma2_load_2d(sa + pair::A_BYTES, &tmB, full + stage, k, n0);
+          if (waited) {
+            pair::tma2_load_3d(sa, &tmA, full + stage, kc, m0, ko);
+          } else {
+            def_stage[n_def] = stage;
+            def_kc[n_def] = kc;
+            def_m[n_def] = m0;
+            def_ko[n_def] = ko;
+            if (++n_def == pair::STAGES) {
+              pdl_wait();
+              waited = true;
+              for (int i = 0; i < n_def; ++i)
+                pair::tma2_load_3d(smem + def_stage[i] * pair::STAGE_BYTES, &tmA, full + def_stage[i], def_kc[i],
+                             def_m[i], def_ko[i]);
+            }
+          }
+          if (++stage == pair::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      if (!waited) {
+        pdl_wait();
+        for (int i = 0; i < n_def; ++i)
+          pair::tma2_load_3d(smem + def_stage[i] * pair::STAGE_BYTES, &tmA, full + def_stage[i], def_kc[i],
+                       def_m[i], def_ko[i]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(256, 256);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      for (int t = cluster; t < p.num_tiles; t += n_clusters) {
+        mbar_wait(tempty + acc, aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(full + stage, phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * pair::STAGE_BYTES);
+          const uint32_t b_addr = a_addr + pair::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            pair::umma2_bf16(d_tmem, sdesc_sw128(a_addr + k * 32), sdesc_sw128(b_addr + k * 32), idesc,
+                       (kb | k) != 0 ? 1u : 0u);
+          pair::umma2_commit_both(empty + stage);
+          if (++stage == pair::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        pair::umma2_commit_both(tfull + acc);
+        if (++acc == ACC_STAGES) {
+          acc = 0;
+          aphase ^= 1;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    pdl_wait();
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t leader_tempty = pair::map_to_rank(smem_u32(tempty), 0);
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int t = cluster; t < p.num_tiles; t += n_clusters) {
+      int mb, nb;
+      tile_coords(t, p, mb, nb);
+      mbar_wait(tfull + acc, aphase);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * 256;
+      const int m = mb * 256 + rank * 128 + row;
+      if (p.epi == SP_EPI_SWIGLU) {
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t g[32], u[32];
+          tmem_ld32(tb + c, g);
+          tmem_ld32(tb + 128 + c, u);
+          tmem_ld_wait();
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = silu(__uint_as_float(g[j])) * __uint_as_float(u[j]);
+          store_chunk(p, m, nb * 128 + c, v, SP_EPI_STORE_BF16, p.N / 2);
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < 256; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tb + c, r);
+          tmem_ld_wait();
+          float v[32];
+          if (p.epi == SP_EPI_GELU) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(__uint_as_float(r[j]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          }
+          store_chunk(p, m, nb * 256 + c, v, p.epi, p.N);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) pair::arrive_remote(pair::map_to_rank(smem_u32(tempty + acc), 0));
+      (void)leader_tempty;
+      if (++acc == ACC_STAGES) {
+        acc = 0;
+        aphase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  pair::cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
 // split-K reduction: v = sum_s ws[s] in ascending s (deterministic), then the
 // epilogue; one thread = 8 consecutive output columns of one row.
 __global__ void splitk_reduce_kernel(const Params p) {
@@ -835,6 +1085,61 @@ static int launch_swap(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   return kOk;
 }
 
+static int launch_pair(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_chunk_stride,
+                       const void* B, int64_t ldb, void* D, int64_t ldd, int M, int N, int K,
+                       int epilogue, int64_t peer_width, int64_t peer_stride, void* stream) {
+  using namespace sp::gemm;
+  CUtensorMap ta, tb;
+  {
+    const uint64_t kin = a_kchunk > 0 ? (uint64_t)a_kchunk : (uint64_t)K;
+    const uint64_t kout = a_kchunk > 0 ? (uint64_t)(K / a_kchunk) : 1;
+    const uint64_t cstride = a_kchunk > 0 ? (uint64_t)a_chunk_stride * 2
+                                          : (uint64_t)lda * 2 * (uint64_t)M;
+    uint64_t dims[3] = {kin, (uint64_t)M, kout};
+    uint64_t strides[2] = {(uint64_t)lda * 2, cstride};
+    uint32_t box[3] = {BK, 128, 1};
+    if (int rc = get_map(&ta, A, 3, dims, strides, box)) return rc;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)K, (uint64_t)N};
+    uint64_t strides[1] = {(uint64_t)ldb * 2};
+    uint32_t box[2] = {BK, 128};
+    if (int rc = get_map(&tb, B, 2, dims, strides, box)) return rc;
+  }
+  Params p;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.num_m = (int)cdiv(M, 256);
+  p.num_n = (int)cdiv(N, 256);
+  p.num_tiles = p.num_m * p.num_n;
+  p.k_blocks = (int)cdiv(K, BK);
+  p.epi = epilogue;
+  p.a_kchunk = (int)(a_kchunk > 0 ? a_kchunk : 0);
+  p.D = D;
+  p.ldd = ldd;
+  p.peer_width = peer_width;
+  p.peer_stride = peer_stride;
+  p.ws = nullptr;
+  p.ksplit = 1;
+  p.kb_per_split = p.k_blocks;
+  {
+    const int64_t a_pair_bytes = (int64_t)256 * K * 2;
+    int64_t gm = (40ll << 20) / std::max<int64_t>(a_pair_bytes, 1);
+    p.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(gm, p.num_m));
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         pair::SMEM_BYTES);
+    attr = true;
+  }
+  const int clusters = std::min(p.num_tiles, sm_count() / 2);
+  launch_k(gemm_pair_kernel, 2 * clusters, NUM_THREADS, pair::SMEM_BYTES,
+           reinterpret_cast<cudaStream_t>(stream), ta, tb, p);
+  return check_launch("gemm_pair_kernel");
+}
+
 // split-K workspace (set once by the host; never allocated in the hot path)
 static float* g_ws = nullptr;
 static int64_t g_ws_bytes = 0;
@@ -908,6 +1213,12 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
   if (const char* f = getenv("SP_GEMM_FORCE_BN")) {
     const int fb = atoi(f);
     if ((fb == 32 || fb == 64 || fb == 128 || fb == 256) && epilogue != SP_EPI_SWIGLU) bn = fb;
+  }
+  if (bn == 256 && M >= 256 && N % 256 == 0) {
+    const char* e = getenv("SP_GEMM_2CTA");
+    if (!(e && e[0] == '0'))
+      return launch_pair(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
+                         peer_width, peer_stride, stream);
   }
   switch (bn) {
     case 256: return launch<256>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue, peer_width, peer_stride, stream);

@@ -386,3 +386,43 @@ def test_gemm_split_k_regime(epi, M):
         assert torch.equal(outs[0], outs[1])
     finally:
         ops.set_gemm_workspace(None)
+
+
+@pytest.mark.parametrize("epi", ["f32", "add", "bf16", "swiglu", "chunked"])
+def test_gemm_cta_pair_large_tiles(epi, monkeypatch):
+    """Large GEMMs run on CTA pairs (tcgen05.mma.cta_group::2, 256x256 tiles);
+    results are bit-identical to the single-CTA kernel and match fp32."""
+    M, N, K = 1000, 8192, 1024
+    a, b = rnd(M, K, seed=50), rnd(N, K, seed=51)
+    ref = a.float() @ b.float().t()
+    outs = {}
+    for pair_on in ("1", "0"):
+        monkeypatch.setenv("SP_GEMM_2CTA", pair_on)
+        if epi == "f32":
+            d = torch.empty(M, N, device="cuda")
+            ops.gemm(a, b, d, ops.EPI_STORE_F32, M=M, N=N, K=K, lda=K, ldb=K, ldd=N)
+            want, tol = ref, 1e-4
+        elif epi == "add":
+            d = torch.full((M, N), 0.5, device="cuda")
+            ops.gemm(a, b, d, ops.EPI_ADD_F32, M=M, N=N, K=K, lda=K, ldb=K, ldd=N)
+            want, tol = ref + 0.5, 1e-4
+        elif epi == "bf16":
+            d = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+            ops.gemm(a, b, d, ops.EPI_STORE_BF16, M=M, N=N, K=K, lda=K, ldb=K, ldd=N)
+            want, tol = ref, 1e-2
+        elif epi == "swiglu":
+            f = N // 2
+            d = torch.empty(M, f, device="cuda", dtype=torch.bfloat16)
+            ops.gemm(a, b, d, ops.EPI_SWIGLU, M=M, N=N, K=K, lda=K, ldb=K, ldd=f)
+            v = ref.view(M, f // 128, 2, 128)
+            want, tol = (torch.nn.functional.silu(v[:, :, 0]) * v[:, :, 1]).reshape(M, f), 1e-2
+        else:
+            P, w = 4, K // 4
+            back = torch.cat([a[:, s * w:(s + 1) * w] for s in range(P)], dim=0).contiguous()
+            d = torch.zeros(M, N, device="cuda")
+            ops.gemm(back, b, d, ops.EPI_ADD_F32, M=M, N=N, K=K, lda=w, ldb=K, ldd=N,
+                     a_kchunk=w, a_chunk_stride=M * w)
+            want, tol = ref, 1e-4
+        assert rel(d, want) < tol, pair_on
+        outs[pair_on] = d
+    assert torch.equal(outs["1"], outs["0"])
