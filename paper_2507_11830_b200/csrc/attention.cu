@@ -149,13 +149,13 @@ __device__ __forceinline__ void softmax_update(float (&s)[KT / 8][4], float (&o)
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
     const float mnew = fmaxf(mrow[h], mx);
     const float msafe = mnew == -INFINITY ? 0.f : mnew;
-    const float corr = exp2f(mrow[h] - msafe);
+    const float corr = fast_exp2(mrow[h] - msafe);
     float sum = 0.f;
 #pragma unroll
     for (int j = 0; j < KT / 8; ++j) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const float pv = exp2f(s[j][2 * h + e] - msafe);
+        const float pv = fast_exp2(s[j][2 * h + e] - msafe);
         s[j][2 * h + e] = pv;
         sum += pv;
       }

@@ -10,7 +10,8 @@
 //   warps 4-7  softmax warpgroup for Q tile 1
 //   warp 8     TMA producer: Q tiles once (3-D map over [tokens][G][d]), then
 //              128-key K/V tiles page by page from the paged pool (2-stage ring)
-//   warp 9     TMEM allocator + single-thread MMA issuer
+//   warp 9     TMEM allocator + single-thread MMA issuer (warps 10-11 idle);
+//              setmaxnreg moves registers from this warpgroup to the softmax ones
 // TMEM (512 cols): S0 | S1 (128 f32 cols each; P_i is written back as bf16 over
 // the first 64 columns of S_i and consumed as the TMEM A-operand of P·V) |
 // O0 | O1 (128 f32 cols each).  MMA issue order per key tile j:
@@ -29,7 +30,7 @@ namespace attn_tc {
 constexpr int HD = 128;
 constexpr int QROWS = 128;       // rows per Q tile
 constexpr int KT = 128;          // keys per tile
-constexpr int NUM_THREADS = 320;
+constexpr int NUM_THREADS = 384;  // 3 warpgroups: softmax 0, softmax 1, producer/MMA
 constexpr int Q_TILE_BYTES = QROWS * HD * 2;      // 32 KiB (two 64-wide d chunks)
 constexpr int KV_TILE_BYTES = KT * HD * 2;        // 32 KiB
 constexpr int SMEM_Q = 2 * Q_TILE_BYTES;
@@ -147,6 +148,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  if (warp >= 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
   if (warp == 8) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
@@ -229,7 +232,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
     __syncwarp();
+  }
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
     // ----------------------------------------------------- softmax warpgroups
     const int t = warp >> 2;            // Q tile
     const int quarter = warp & 3;       // TMEM lane quarter
@@ -245,14 +250,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int j = 0; j < n_kt; ++j) {
       mbar_wait(s_full + t, j & 1);
       tc_fence_after();
-      float s[KT];
+      float s[KT];  // raw scores; the softmax scale is folded into one FFMA below
 #pragma unroll
       for (int c = 0; c < KT / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(s_tmem + c * 32, r);
         tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(r[e]) * p.scale_log2;
+        for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(r[e]);
       }
       const int kbase = j * KT;
       if (kbase + KT - 1 > limit) {
@@ -263,11 +268,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       float mx = -INFINITY;
 #pragma unroll
       for (int e = 0; e < KT; ++e) mx = fmaxf(mx, s[e]);
-      const float m_new = fmaxf(m_run, mx);
+      const float m_new = fmaxf(m_run, mx * p.scale_log2);
       const bool need = m_new > m_run + kRescaleThreshold;
       float corr = 1.f;
       if (need) {
-        corr = exp2f(m_run - m_new);
+        corr = fast_exp2(m_run - m_new);
         m_run = m_new;
       }
       l_run *= corr;
@@ -283,20 +288,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         tmem_st_wait();
       }
-      float sum = 0.f;
+      // p = 2^(raw * scale - m_run): FFMA2 + 2 x MUFU.EX2 + FADD2 per pair
+      const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2);
+      const uint64_t nm2 = f2_pack(-m_run, -m_run);
+      uint64_t sum2 = f2_pack(0.f, 0.f);
 #pragma unroll
       for (int c = 0; c < KT / 64; ++c) {
         uint32_t pk[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          const float a = exp2f(s[c * 64 + 2 * e] - m_run);
-          const float b = exp2f(s[c * 64 + 2 * e + 1] - m_run);
-          sum += a + b;
+          float a, b;
+          f2_unpack(f2_fma(f2_pack(s[c * 64 + 2 * e], s[c * 64 + 2 * e + 1]), sc2, nm2), a, b);
+          a = fast_exp2(a);
+          b = fast_exp2(b);
+          sum2 = f2_add(sum2, f2_pack(a, b));
           pk[e] = pack_bf16x2(a, b);
         }
         tmem_st32(s_tmem + c * 32, pk);
       }
-      l_run += sum;
+      float sa, sb;
+      f2_unpack(sum2, sa, sb);
+      l_run += sa + sb;
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(p_full + t);
