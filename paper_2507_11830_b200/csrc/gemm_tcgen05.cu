@@ -86,7 +86,12 @@ __device__ __forceinline__ float gelu_tanh(float x) {
   return 0.5f * x * (1.f + tanhf(c * (x + k * x * x * x)));
 }
 
-__device__ __forceinline__ float silu(float x) { return x / (1.f + __expf(-x)); }
+// x * sigmoid(x) with SFU ex2 + rcp (no IEEE division sequence)
+__device__ __forceinline__ float silu(float x) {
+  float e = fast_exp2(-1.4426950408889634f * x), r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.f + e));
+  return x * r;
+}
 
 // one thread: 32 consecutive columns [n0, n0+32) of row m
 __device__ __forceinline__ void store_chunk(const Params& p, int m, int n0, const float (&v)[32],

@@ -1,0 +1,3 @@
+timeout 300 python -m pytest tests/test_kernels_gpu.py -q -m gpu -x -k "swiglu or split_k or cta_pair" > gpurun_out/kt.log 2>&1; echo "kt exit $?" >> gpurun_out/kt.log
+timeout 300 python tools/kbench.py gemm > gpurun_out/kbench.log 2>&1; echo "kb exit $?" >> gpurun_out/kbench.log
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench exit $?" >> gpurun_out/bench.log

@@ -53,6 +53,8 @@ def gemm_cases():
     for name, m, n, k, epi in [("qkv", M, qkv, h, ops.EPI_STORE_BF16),
                                 ("o", M, h, h, ops.EPI_ADD_F32),
                                 ("gate_up", M, 2 * f, h, ops.EPI_SWIGLU),
+                                ("gate_up_plain_bf16", M, 2 * f, h, ops.EPI_STORE_BF16),
+                                ("n28672_k4096_f32", M, 2 * f, h, ops.EPI_STORE_F32),
                                 ("down", M, h, f, ops.EPI_ADD_F32),
                                 ("square8k", 8192, 8192, 8192, ops.EPI_STORE_BF16),
                                 ("decode_qkv_b64", 64, qkv, h, ops.EPI_STORE_BF16),
