@@ -111,9 +111,53 @@ def swiftkv(weights, cfg, seq=32768, cut=16):
           flush=True)
 
 
+def model_70b(seq=8192, dec_b=16, ctx=2048):
+    """configs[3] model geometry on ONE B200: Llama-3.3-70B bf16 replica (141 GB):
+    8K single-request prefill tok/s and decode TPOT at B=16, ctx 2K."""
+    from paper_2507_11830_b200 import llama33_70b
+    cfg = llama33_70b(max_seq=max(seq, ctx + 64))
+    w = ModelWeights.random(cfg, seed=0, world_size=1)
+    rng = np.random.default_rng(2)
+    blocks = -(-seq // 64) + dec_b * -(-(ctx + 64) // 64) + 8
+    eng = Engine(w, LoopbackGroup(1), ShiftPolicy.fixed_sp(), num_blocks=blocks)
+    prompt = [int(t) for t in rng.integers(0, cfg.vocab_size, size=seq)]
+    s = eng.new_sequence(0, capacity=seq)
+    batch = Batch(BatchKind.PREFILL, [BatchItem(s, prompt)])
+
+    def pre():
+        s.cache.truncate(0)
+        eng.step(batch, mode=ParallelMode.SP)
+    ms = timed(pre, 3, warm=1)
+    gemm_fl = gemm_flops_per_token(cfg) * seq
+    attn_fl = causal_attention_flops(cfg, [seq], [0])
+    seqs = [eng.new_sequence(10 + i, capacity=ctx + 64) for i in range(dec_b)]
+    for i in range(0, dec_b, 4):
+        eng.step(Batch(BatchKind.PREFILL, [BatchItem(q, [int(t) for t in rng.integers(0, 1000, ctx)])
+                                           for q in seqs[i:i + 4]]), mode=ParallelMode.SP)
+
+    def dec():
+        for q in seqs:
+            q.cache.truncate(ctx)
+        eng.step(Batch(BatchKind.DECODE, [BatchItem(q, [1]) for q in seqs]), mode=ParallelMode.TP)
+    tpot = timed(dec, 8, warm=3)
+    wbytes = w.nbytes()
+    kv = dec_b * ctx * cfg.n_layers * 2 * cfg.kv_heads * cfg.head_dim * 2
+    roof = (wbytes + kv) / (PEAKS["hbm_gbs"] * 1e9) * 1e3
+    print(json.dumps({"config": "llama-3.3-70b geometry on 1x B200 (configs[3] model)",
+                      "weights_gb": round(wbytes / 1e9, 1), "prefill_seq": seq,
+                      "prefill_ms": round(ms, 2), "prefill_tokens_per_s": round(seq / ms * 1e3, 1),
+                      "prefill_tflops": round((gemm_fl + attn_fl) / (ms / 1e3) / 1e12, 1),
+                      "decode_batch": dec_b, "decode_ctx": ctx, "tpot_ms": round(tpot, 3),
+                      "decode_hbm_roofline_ms": round(roof, 3),
+                      "decode_frac_of_roofline": round(roof / tpot, 4)}), flush=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     torch.cuda.set_device(0)
+    if what == "70b":
+        model_70b()
+        sys.exit(0)
     cfg = llama31_8b(max_seq=32768 + 64)
     weights = ModelWeights.random(cfg, seed=0, world_size=1)
     if what in ("decode-sweep", "all"):
