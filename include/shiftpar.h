@@ -146,6 +146,30 @@ sp_status sp_a2a_pack(const void* src, int64_t lds, void* dst, int rows, int pee
 sp_status sp_a2a_unpack(const void* src, void* dst, int64_t ldd, int rows, int peers,
                         int width, void* stream);
 
+/* ---------------------------------- fused all-to-all over peer memory
+ * The SP re-shards without a collective library on the data path:
+ *  - seq->head (parallel_engine.py:485-487): the QKV GEMM stores column block
+ *    b = n / peer_width of row m straight into peer b's receive buffer,
+ *    peer_ptrs[b] + (row_off + m) * ldd + (n % peer_width)  (device array of
+ *    P peer pointers — NVLink addresses via symmetric memory, or in-process
+ *    buffers for loopback ranks);
+ *  - head->seq (:503-509): row t of src [rows_total, width] goes to its owner
+ *    s's buffer dst_ptrs[s] at row my_rank * rows_s + (t - lo_s), i.e. the
+ *    [P][rows_s][width] layout the O-projection reads through a chunked-K map;
+ *  - completion: sp_peer_signal sets flag slot [my_rank] in every peer's flag
+ *    array (system-scope release after the stores), sp_peer_wait acquires all
+ *    P local flags and resets them.
+ */
+sp_status sp_gemm_bf16_to_peers(const void* A, int64_t lda, int64_t a_kchunk,
+                                int64_t a_chunk_stride, const void* B, int64_t ldb,
+                                const unsigned long long* peer_ptrs, int64_t row_off,
+                                int64_t ldd, int M, int N, int K, int epilogue,
+                                int64_t peer_width, void* stream);
+sp_status sp_peer_scatter_rows(const void* src, int64_t lds, int rows_total, int width, int peers,
+                               int my_rank, const unsigned long long* dst_ptrs, void* stream);
+sp_status sp_peer_signal(const unsigned long long* flag_ptrs, int peers, int my_rank, void* stream);
+sp_status sp_peer_wait(int* flags, int peers, void* stream);
+
 /* ---------------------------------------------- reductions and heads
  * In-process (loopback) all-reduce: dst = a + b, f32, ascending order as in
  * DeviceGroup.all_reduce_sum (fabric.py:117-143).

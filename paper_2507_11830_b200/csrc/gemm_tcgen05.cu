@@ -28,6 +28,10 @@
 namespace sp {
 namespace gemm {
 
+// per-call peer target of sp_gemm_bf16_to_peers (host thread-local)
+static thread_local const unsigned long long* t_peer_ptrs = nullptr;
+static thread_local int64_t t_peer_row_off = 0;
+
 constexpr int BM = 128, BK = 64, ACC_STAGES = 2;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int NUM_THREADS = 192;
@@ -60,7 +64,29 @@ struct Params {
   int ksplit, kb_per_split;
   float* ws;
   int group_m;  // m-tiles per raster group (A rows of a group stay L2-resident)
+  // fused all-to-all: column block b = n / peer_width goes to peer b's buffer
+  // peer_ptrs[b] at row (m + peer_row_off) — stores cross NVLink directly
+  const unsigned long long* peer_ptrs;
+  int64_t peer_row_off;
 };
+
+// destination element (m, n) of D honouring the per-peer layouts
+template <typename T>
+__device__ __forceinline__ T* out_ptr(const Params& p, int m, int64_t n) {
+  T* base = reinterpret_cast<T*>(p.D);
+  int64_t col = n, row = m, off = 0;
+  if (p.peer_width > 0) {
+    const int64_t peer = n / p.peer_width;
+    col = n - peer * p.peer_width;
+    if (p.peer_ptrs != nullptr) {
+      base = reinterpret_cast<T*>(p.peer_ptrs[peer]);
+      row = m + p.peer_row_off;
+    } else {
+      off = peer * p.peer_stride;
+    }
+  }
+  return base + off + row * p.ldd + col;
+}
 
 __device__ __forceinline__ void tile_coords(int t, const Params& p, int& mb, int& nb) {
   const int per_group = p.group_m * p.num_n;
@@ -98,15 +124,8 @@ __device__ __forceinline__ void store_chunk(const Params& p, int m, int n0, cons
                                             int epi, int N) {
   if (m >= p.M || n0 >= N) return;
   const int ncols = min(32, N - n0);
-  int64_t col = n0;
-  int64_t base = 0;
-  if (p.peer_width > 0) {
-    const int64_t peer = n0 / p.peer_width;
-    col = n0 - peer * p.peer_width;
-    base = peer * p.peer_stride;
-  }
   if (epi == SP_EPI_STORE_BF16 || epi == SP_EPI_GELU) {
-    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.D) + base + (int64_t)m * p.ldd + col;
+    __nv_bfloat16* dst = out_ptr<__nv_bfloat16>(p, m, n0);
     if (ncols == 32) {
       uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
@@ -124,7 +143,7 @@ __device__ __forceinline__ void store_chunk(const Params& p, int m, int n0, cons
         if (j < ncols) dst[j] = __float2bfloat16_rn(v[j]);
     }
   } else {
-    float* dst = reinterpret_cast<float*>(p.D) + base + (int64_t)m * p.ldd + col;
+    float* dst = out_ptr<float>(p, m, n0);
     if (ncols == 32) {
       float4* d4 = reinterpret_cast<float4*>(dst);
       if (epi == SP_EPI_ADD_F32) {
@@ -522,25 +541,18 @@ __global__ void __launch_bounds__(NUM_THREADS, SwapTile<NT>::CTAS_PER_SM)
             for (int j = 0; j < 32; ++j)
               if (c + j < p.M) dst[(int64_t)(c + j) * p.N] = __uint_as_float(r[j]);
           } else {
-            int64_t col = n, base = 0;
-            if (p.peer_width > 0) {
-              const int64_t peer = n / p.peer_width;
-              col = n - peer * p.peer_width;
-              base = peer * p.peer_stride;
-            }
 #pragma unroll 4
             for (int j = 0; j < 32; ++j) {
               const int m = c + j;
               if (m >= p.M) break;
               float v = __uint_as_float(r[j]);
-              const int64_t off = base + (int64_t)m * p.ldd + col;
               if (p.epi == SP_EPI_STORE_F32) {
-                reinterpret_cast<float*>(p.D)[off] = v;
+                *out_ptr<float>(p, m, n) = v;
               } else if (p.epi == SP_EPI_ADD_F32) {
-                reinterpret_cast<float*>(p.D)[off] += v;
+                *out_ptr<float>(p, m, n) += v;
               } else {
                 if (p.epi == SP_EPI_GELU) v = gelu_tanh(v);
-                reinterpret_cast<__nv_bfloat16*>(p.D)[off] = __float2bfloat16_rn(v);
+                *out_ptr<__nv_bfloat16>(p, m, n) = __float2bfloat16_rn(v);
               }
             }
           }
@@ -858,15 +870,8 @@ __global__ void splitk_reduce_kernel(const Params p) {
       for (int j = 0; j < 8; ++j) v[j] = gelu_tanh(v[j]);
     }
   }
-  int64_t col = c, base = 0;
-  if (p.peer_width > 0) {
-    const int64_t peer = c / p.peer_width;
-    col = c - peer * p.peer_width;
-    base = peer * p.peer_stride;
-  }
   if (p.epi == SP_EPI_STORE_F32 || p.epi == SP_EPI_ADD_F32) {
-    float* dst = reinterpret_cast<float*>(p.D) + base + (int64_t)m * p.ldd + col;
-    float4* d4 = reinterpret_cast<float4*>(dst);
+    float4* d4 = reinterpret_cast<float4*>(out_ptr<float>(p, m, c));
     if (p.epi == SP_EPI_ADD_F32) {
       float4 x0 = d4[0], x1 = d4[1];
       d4[0] = make_float4(x0.x + v[0], x0.y + v[1], x0.z + v[2], x0.w + v[3]);
@@ -876,7 +881,7 @@ __global__ void splitk_reduce_kernel(const Params p) {
       d4[1] = make_float4(v[4], v[5], v[6], v[7]);
     }
   } else {
-    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.D) + base + (int64_t)m * p.ldd + col;
+    __nv_bfloat16* dst = out_ptr<__nv_bfloat16>(p, m, c);
     uint4 u;
     u.x = pack_bf16x2(v[0], v[1]);
     u.y = pack_bf16x2(v[2], v[3]);
@@ -977,6 +982,8 @@ static int launch(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_chunk_
     if (int rc = get_map(&tb, B, 2, dims, strides, box)) return rc;
   }
   Params p;
+  p.peer_ptrs = t_peer_ptrs;
+  p.peer_row_off = t_peer_row_off;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -1055,6 +1062,8 @@ static int launch_swap(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
     if (int rc = get_map(&tw, B, 2, dims, strides, box)) return rc;
   }
   Params p;
+  p.peer_ptrs = t_peer_ptrs;
+  p.peer_row_off = t_peer_row_off;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -1112,6 +1121,8 @@ static int launch_pair(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
     if (int rc = get_map(&tb, B, 2, dims, strides, box)) return rc;
   }
   Params p;
+  p.peer_ptrs = t_peer_ptrs;
+  p.peer_row_off = t_peer_row_off;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -1231,4 +1242,25 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
     case 64: return launch<64>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue, peer_width, peer_stride, stream);
     default: return launch<32>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue, peer_width, peer_stride, stream);
   }
+}
+
+extern "C" sp_status sp_gemm_bf16_to_peers(const void* A, int64_t lda, int64_t a_kchunk,
+                                           int64_t a_chunk_stride, const void* B, int64_t ldb,
+                                           const unsigned long long* peer_ptrs, int64_t row_off,
+                                           int64_t ldd, int M, int N, int K, int epilogue,
+                                           int64_t peer_width, void* stream) {
+  using namespace sp::gemm;
+  if (!peer_ptrs || peer_width <= 0 || N % peer_width)
+    return fail(kInvalid, "gemm_to_peers: need peer pointers and N % peer_width == 0");
+  if (epilogue != SP_EPI_STORE_BF16 && epilogue != SP_EPI_STORE_F32)
+    return fail(kUnsupported, "gemm_to_peers: store epilogues only");
+  t_peer_ptrs = peer_ptrs;
+  t_peer_row_off = row_off;
+  // D is never dereferenced in peer mode; pass an aligned placeholder for validation
+  const int rc = sp_gemm_bf16(A, lda, a_kchunk, a_chunk_stride, B, ldb,
+                              reinterpret_cast<void*>(const_cast<unsigned long long*>(peer_ptrs)),
+                              ldd, M, N, K, epilogue, peer_width, 0, stream);
+  t_peer_ptrs = nullptr;
+  t_peer_row_off = 0;
+  return rc;
 }

@@ -42,6 +42,7 @@ from .errors import CacheOverflow, ConfigError, ContractViolation
 from .fabric import CommRecord, DeviceGroup, LoopbackGroup
 from .flops import FlopMeter, PassShape, flop_count, shard_bounds, shard_rows
 from .kv_cache import KvCache, KvPool
+from .peer import PeerLinks, fused_a2a_enabled
 from .weights import ModelWeights
 
 
@@ -206,7 +207,7 @@ class _GraphEntry:
 class Engine:
     def __init__(self, weights: ModelWeights, group: DeviceGroup, policy: ShiftPolicy,
                  swiftkv: Optional[SwiftKvConfig] = None, *, num_blocks: Optional[int] = None,
-                 block_size: int = 64, cuda_graphs: bool = True):
+                 block_size: int = 64, cuda_graphs: bool = True, max_pass_tokens: int = 16384):
         cfg = weights.config
         self.weights = weights
         self.config: ModelConfig = cfg
@@ -233,6 +234,11 @@ class Engine:
             num_blocks = max(16, 4 * -(-cfg.max_seq // block_size))
         self.pool = KvPool(cfg.n_layers, self.kv_partition, cfg.head_dim, num_blocks, block_size,
                            group.local_ranks, self.device)
+        # fused SP all-to-all over peer memory (passes up to max_pass_tokens tokens)
+        self._peer: Optional[PeerLinks] = None
+        if fused_a2a_enabled(group):
+            hqw = cfg.n_heads // self.world_size * cfg.head_dim
+            self._peer = PeerLinks(group, max_pass_tokens, weights.qkv_width, hqw, self.device)
         self.mode_log: List[ParallelMode] = []
         self.step_records: List[StepRecord] = []
         self._step_counter = 0
@@ -750,13 +756,21 @@ class Engine:
         n_full = cfg.n_layers if cut is None else cut
         in_fwd = {r: [rows[r]] * P for r in range(P)}
         out_fwd = {s: list(rows) for s in range(P)}
+        peer = self._peer if (self._peer is not None and M <= self._peer.max_tokens) else None
         for layer in range(n_full):
             lw = w.layers[layer]
             send, recv = {}, {}
             for r in g.local_ranks:
                 xn = torch.empty((rows[r], h), dtype=torch.bfloat16, device=dev)
                 ops.add_rmsnorm(xs[r], lw.attn_gain, eps, xn)
-                if P == 1:
+                if peer is not None:
+                    # fused seq->head all-to-all: the epilogue stores rank s's q|k|v
+                    # heads straight into s's receive buffer at this shard's rows
+                    ops.gemm_to_peers(xn, lw.wqkv, peer.recv_ptrs, row_off=bounds[r][0],
+                                      M=rows[r], N=P * W, K=h, lda=h, ldb=h, ldd=W,
+                                      peer_width=W, meter=meters[r])
+                    ops.peer_signal(peer.fwd_flag_ptrs, P, r)
+                elif P == 1:
                     send[r] = torch.empty((M, W), dtype=torch.bfloat16, device=dev)
                     ops.gemm(xn, lw.wqkv, send[r], ops.EPI_STORE_BF16, M=M, N=W, K=h, lda=h,
                              ldb=h, ldd=W, meter=meters[r])
@@ -768,7 +782,12 @@ class Engine:
                              lda=h, ldb=h, ldd=W, peer_width=W, peer_stride=rows[r] * W,
                              meter=meters[r])
                     recv[r] = torch.empty((M, W), dtype=torch.bfloat16, device=dev)
-            if P > 1:
+            if peer is not None:
+                g._charge_a2a(in_fwd, W * 2)
+                for r in g.local_ranks:
+                    ops.peer_wait(peer.flags[r][0], P)
+                    recv[r] = peer.recv[r][:M]
+            elif P > 1:
                 g.all_to_all(send, recv, in_fwd, out_fwd, row_bytes=W * 2)
             self._stage_all(layer, batch)
             att = {}
@@ -779,7 +798,17 @@ class Engine:
                 self._attend(r, layer, q, o, meta, meters[r])
                 att[r] = o
             back = att
-            if P > 1:
+            if peer is not None:
+                # fused head->seq all-to-all: rows go straight to their owner's buffer
+                for r in g.local_ranks:
+                    ops.peer_scatter_rows(att[r], M, P, r, peer.back_ptrs)
+                    ops.peer_signal(peer.back_flag_ptrs, P, r)
+                g._charge_a2a({r: list(rows) for r in range(P)}, hqw * 2)
+                back = {}
+                for r in g.local_ranks:
+                    ops.peer_wait(peer.flags[r][1], P)
+                    back[r] = peer.back[r][:P * rows[r]]
+            elif P > 1:
                 back = {r: torch.empty((P * rows[r], hqw), dtype=torch.bfloat16, device=dev)
                         for r in g.local_ranks}
                 g.all_to_all(att, back, {r: list(rows) for r in range(P)},

@@ -126,6 +126,48 @@ def set_gemm_workspace(ws: Optional[torch.Tensor]) -> None:
     _lib.check(_lib.load().sp_gemm_set_workspace(_ptr(ws), nbytes), "sp_gemm_set_workspace")
 
 
+def gemm_to_peers(a: torch.Tensor, b: torch.Tensor, peer_ptrs: torch.Tensor, *, row_off: int,
+                  M: int, N: int, K: int, lda: int, ldb: int, ldd: int, peer_width: int,
+                  epilogue: int = EPI_STORE_BF16, a_kchunk: int = 0, a_chunk_stride: int = 0,
+                  meter=None) -> None:
+    """GEMM whose epilogue stores column block n // peer_width of row m straight
+    into peer_ptrs[block] at row row_off + m (fused seq->head all-to-all)."""
+    _need(a, torch.bfloat16, "gemm A")
+    _need(b, torch.bfloat16, "gemm B")
+    if meter is not None:
+        meter.add_matmul(M, K, N)
+    if M == 0:
+        return
+    with _Timed("gemm", 2 * M * N * K, (M * K + N * K) * 2 + M * N * 2):
+        rc = _lib.load().sp_gemm_bf16_to_peers(a.data_ptr(), lda, a_kchunk, a_chunk_stride,
+                                               b.data_ptr(), ldb, peer_ptrs.data_ptr(), row_off,
+                                               ldd, M, N, K, epilogue, peer_width, _stream())
+    _lib.check(rc, "sp_gemm_bf16_to_peers")
+    _count()
+
+
+def peer_scatter_rows(src: torch.Tensor, rows_total: int, peers: int, my_rank: int,
+                      dst_ptrs: torch.Tensor) -> None:
+    """Row t of src goes to its SP owner's [P][rows_s][w] buffer (head->seq)."""
+    if rows_total == 0:
+        return
+    _lib.check(_lib.load().sp_peer_scatter_rows(src.data_ptr(), src.stride(0), rows_total,
+                                                src.shape[1], peers, my_rank, dst_ptrs.data_ptr(),
+                                                _stream()), "sp_peer_scatter_rows")
+    _count()
+
+
+def peer_signal(flag_ptrs: torch.Tensor, peers: int, my_rank: int) -> None:
+    _lib.check(_lib.load().sp_peer_signal(flag_ptrs.data_ptr(), peers, my_rank, _stream()),
+               "sp_peer_signal")
+    _count()
+
+
+def peer_wait(flags: torch.Tensor, peers: int) -> None:
+    _lib.check(_lib.load().sp_peer_wait(flags.data_ptr(), peers, _stream()), "sp_peer_wait")
+    _count()
+
+
 def embed(ids: torch.Tensor, table: torch.Tensor, out: torch.Tensor,
           pos: Optional[torch.Tensor] = None, pos_table: Optional[torch.Tensor] = None) -> None:
     _need(ids, torch.int32, "embed ids")

@@ -1,0 +1,92 @@
+"""Static peer buffers for the fused SP all-to-all (no collective on the data path).
+
+Each rank owns, at addresses every peer knows:
+  recv  bf16 [max_tokens, W]           seq->head receive (QKV GEMM epilogue stores here)
+  back  bf16 [P * rows_max, hq_l * d]  head->seq receive ([P][rows][w], O-proj A operand)
+  flags int32 [2, P]                   completion flags (fwd, back), one slot per sender
+
+Device tables of the P peers' addresses feed the kernels (sp_gemm_bf16_to_peers,
+sp_peer_scatter_rows, sp_peer_signal).  In-process ranks (LoopbackGroup) use
+plain buffers on the one device; across GPUs the buffers live in one
+torch symmetric-memory allocation per rank whose peer mappings are NVLink
+addresses (opt-in with SP_FUSED_A2A=1 until validated on a multi-GPU box).
+"""
+
+from __future__ import annotations
+
+import os
+from typing import Dict, List
+
+import torch
+
+from .fabric import DeviceGroup, LoopbackGroup
+
+
+def _align(n: int, a: int = 256) -> int:
+    return -(-n // a) * a
+
+
+class PeerLinks:
+    def __init__(self, group: DeviceGroup, max_tokens: int, width_qkv: int, width_back: int,
+                 device: torch.device):
+        P = group.world_size
+        self.P = P
+        self.max_tokens = max_tokens
+        self.rows_max = -(-max_tokens // P)
+        self.W = width_qkv
+        self.w_back = width_back
+        n_recv = max_tokens * width_qkv * 2
+        n_back = P * self.rows_max * width_back * 2
+        n_flag = 2 * P * 4
+        self.off_recv, self.off_back = 0, _align(n_recv)
+        self.off_flags = self.off_back + _align(n_back)
+        total = self.off_flags + _align(n_flag)
+        self.recv: Dict[int, torch.Tensor] = {}
+        self.back: Dict[int, torch.Tensor] = {}
+        self.flags: Dict[int, torch.Tensor] = {}
+        bases: List[int] = [0] * P
+        if isinstance(group, LoopbackGroup):
+            self._bufs = {}
+            for r in range(P):
+                buf = torch.zeros(total, dtype=torch.uint8, device=device)
+                self._bufs[r] = buf
+                bases[r] = buf.data_ptr()
+                self._views(r, buf)
+        else:  # one symmetric allocation per rank; peers map it over NVLink
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+            buf = symm_mem.empty(total, dtype=torch.uint8, device=device)
+            buf.zero_()
+            hdl = symm_mem.rendezvous(buf, dist.group.WORLD.group_name)
+            self._bufs = {group.rank: buf}
+            self._hdl = hdl
+            bases = list(hdl.buffer_ptrs)
+            self._views(group.rank, buf)
+            torch.cuda.synchronize()
+            dist.barrier()
+
+        def table(off: int) -> torch.Tensor:
+            return torch.tensor([b + off for b in bases], dtype=torch.int64, device=device)
+
+        self.recv_ptrs = table(self.off_recv)
+        self.back_ptrs = table(self.off_back)
+        self.fwd_flag_ptrs = table(self.off_flags)
+        self.back_flag_ptrs = table(self.off_flags + P * 4)
+
+    def _views(self, r: int, buf: torch.Tensor) -> None:
+        P = self.P
+        self.recv[r] = buf[self.off_recv:self.off_recv + self.max_tokens * self.W * 2] \
+            .view(torch.bfloat16).view(self.max_tokens, self.W)
+        nb = P * self.rows_max * self.w_back
+        self.back[r] = buf[self.off_back:self.off_back + nb * 2].view(torch.bfloat16) \
+            .view(P * self.rows_max, self.w_back)
+        self.flags[r] = buf[self.off_flags:self.off_flags + 2 * P * 4].view(torch.int32).view(2, P)
+
+
+def fused_a2a_enabled(group: DeviceGroup) -> bool:
+    if group.world_size < 2:
+        return False
+    env = os.environ.get("SP_FUSED_A2A")
+    if isinstance(group, LoopbackGroup):
+        return env != "0"
+    return env == "1"

@@ -396,3 +396,30 @@ def test_cuda_graph_decode_matches_eager(c1, p):
     for a, b in zip(o0, o1):
         for x, y in zip(a, b):
             assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_fused_peer_all_to_all_matches_collective_path(c1_kv4, p, monkeypatch):
+    """The fused SP all-to-all (QKV epilogue storing into peers' receive buffers,
+    attention rows scattered to owners, device flags) gives bit-identical logits
+    and the same comm ledger as the collective path."""
+    prompts = [c1_prompts()[i] for i in (1, 4, 6)]
+    res = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("SP_FUSED_A2A", fused)
+        eng = make(c1_kv4, p)
+        assert (eng._peer is not None) == (fused == "1")
+        seqs = [eng.new_sequence(i, capacity=200) for i in range(3)]
+        lg, rec = eng.step(Batch(BatchKind.PREFILL, [BatchItem(s, q) for s, q in zip(seqs, prompts)]),
+                           mode=ParallelMode.SP, span_logits=True)
+        out = [x.cpu() for x in lg]
+        recs = [rec.comm]
+        for step in range(3):  # decode (graph-captured after the first pass)
+            lg, rec = eng.step(Batch(BatchKind.DECODE, [BatchItem(s, [5 + step]) for s in seqs]),
+                               mode=ParallelMode.SP)
+            out += [x.cpu() for x in lg]
+            recs.append(rec.comm)
+        res[fused] = (out, recs)
+    for a, b in zip(res["1"][0], res["0"][0]):
+        assert torch.equal(a, b)
+    assert res["1"][1] == res["0"][1]
