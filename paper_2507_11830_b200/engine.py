@@ -238,7 +238,8 @@ class Engine:
         self._peer: Optional[PeerLinks] = None
         if fused_a2a_enabled(group):
             hqw = cfg.n_heads // self.world_size * cfg.head_dim
-            self._peer = PeerLinks(group, max_pass_tokens, weights.qkv_width, hqw, self.device)
+            self._peer = PeerLinks(group, max_pass_tokens, weights.qkv_width, hqw, cfg.hidden,
+                                   self.device)
         self.mode_log: List[ParallelMode] = []
         self.step_records: List[StepRecord] = []
         self._step_counter = 0
@@ -582,9 +583,15 @@ class Engine:
         pending: Optional[torch.Tensor] = None
         n_full = cfg.n_layers if cut is None else cut
         xn = torch.empty((M, h), dtype=torch.bfloat16, device=dev)
+        # fused one-shot all-reduce over peer memory (partials -> peers' sum in the norm kernel)
+        peer = self._peer if (self._peer is not None and M <= self._peer.max_tokens) else None
+        peer_pending = False
         for layer in range(n_full):
             lw = w.layers[layer]
-            ops.add_rmsnorm(x, lw.attn_gain, eps, xn, add=pending)
+            if peer_pending:
+                ops.peer_allreduce_add_rmsnorm(peer.part_ptrs[1], P, x, lw.attn_gain, eps, xn, M)
+            else:
+                ops.add_rmsnorm(x, lw.attn_gain, eps, xn, add=pending)
             self._stage_all(layer, batch)
             parts = {}
             for r in g.local_ranks:
@@ -600,13 +607,20 @@ class Engine:
                     ops.gemm(o, wo, x, ops.EPI_ADD_F32, M=M, N=h, K=hqw, lda=hqw,
                              ldb=cfg.n_heads * d, ldd=h, meter=meters[r])
                 else:
-                    part = torch.empty((M, h), dtype=torch.float32, device=dev)
+                    part = (peer.part[r][0][:M] if peer is not None
+                            else torch.empty((M, h), dtype=torch.float32, device=dev))
                     ops.gemm(o, wo, part, ops.EPI_STORE_F32, M=M, N=h, K=hqw, lda=hqw,
                              ldb=cfg.n_heads * d, ldd=h, meter=meters[r])
                     parts[r] = part
-            red = g.all_reduce_sum(parts)[g.local_ranks[0]] if P > 1 else None
+                    if peer is not None:
+                        ops.peer_signal(peer.tp_flag_ptrs[0], P, r)
             xn2 = torch.empty((M, h), dtype=torch.bfloat16, device=dev)
-            ops.add_rmsnorm(x, lw.mlp_gain, eps, xn2, add=red)
+            if peer is not None:
+                self._peer_reduce_wait(0, parts)
+                ops.peer_allreduce_add_rmsnorm(peer.part_ptrs[0], P, x, lw.mlp_gain, eps, xn2, M)
+            else:
+                red = g.all_reduce_sum(parts)[g.local_ranks[0]] if P > 1 else None
+                ops.add_rmsnorm(x, lw.mlp_gain, eps, xn2, add=red)
             parts = {}
             for r in g.local_ranks:
                 act = torch.empty((M, fl), dtype=torch.bfloat16, device=dev)
@@ -616,12 +630,21 @@ class Engine:
                     ops.gemm(act, wd, x, ops.EPI_ADD_F32, M=M, N=h, K=fl, lda=fl,
                              ldb=cfg.ffn_dim, ldd=h, meter=meters[r])
                 else:
-                    part = torch.empty((M, h), dtype=torch.float32, device=dev)
+                    part = (peer.part[r][1][:M] if peer is not None
+                            else torch.empty((M, h), dtype=torch.float32, device=dev))
                     ops.gemm(act, wd, part, ops.EPI_STORE_F32, M=M, N=h, K=fl, lda=fl,
                              ldb=cfg.ffn_dim, ldd=h, meter=meters[r])
                     parts[r] = part
-            pending = g.all_reduce_sum(parts)[g.local_ranks[0]] if P > 1 else None
-        if pending is not None:
+                    if peer is not None:
+                        ops.peer_signal(peer.tp_flag_ptrs[1], P, r)
+            if peer is not None:
+                self._peer_reduce_wait(1, parts)
+                peer_pending = True
+            else:
+                pending = g.all_reduce_sum(parts)[g.local_ranks[0]] if P > 1 else None
+        if peer_pending:
+            ops.peer_allreduce_add_rmsnorm(peer.part_ptrs[1], P, x, None, eps, None, M)
+        elif pending is not None:
             ops.add_f32(x, pending, x)
         if cut is not None:
             x_rows, n_rows = self._tail_tp(meta, batch, meters, x, cut), meta.n
@@ -643,6 +666,14 @@ class Engine:
             parts[r] = lg
         logits = self._gather_vocab(parts, n_rows)
         return self._split(logits, meta, span_logits and cut is None)
+
+    def _peer_reduce_wait(self, which: int, parts: Dict[int, torch.Tensor]) -> None:
+        """Ledger + completion wait of a fused TP all-reduce (flag rows 2/3)."""
+        g, P, peer = self.group, self.world_size, self._peer
+        t = next(iter(parts.values()))
+        g.charge("all_reduce", [2.0 * (P - 1) / P * t.numel() * t.element_size()] * P)
+        for r in g.local_ranks:
+            ops.peer_wait(peer.flags[r][2 + which], P)
 
     def _mlp_up(self, xn2, lw, r, act, rows, meter):
         cfg = self.config

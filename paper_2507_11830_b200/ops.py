@@ -168,6 +168,19 @@ def peer_wait(flags: torch.Tensor, peers: int) -> None:
     _count()
 
 
+def peer_allreduce_add_rmsnorm(part_ptrs: torch.Tensor, peers: int, x: torch.Tensor,
+                               gain: Optional[torch.Tensor], eps: float,
+                               out: Optional[torch.Tensor], rows: int) -> None:
+    """x += sum of the P peer partials (ascending rank), then optional RMSNorm."""
+    if rows == 0:
+        return
+    _lib.check(_lib.load().sp_peer_allreduce_add_rmsnorm(
+        part_ptrs.data_ptr(), peers, x.data_ptr(), x.stride(0), _ptr(gain), float(eps), _ptr(out),
+        0 if out is None else out.stride(0), rows, x.shape[1], _stream()),
+        "sp_peer_allreduce_add_rmsnorm")
+    _count()
+
+
 def embed(ids: torch.Tensor, table: torch.Tensor, out: torch.Tensor,
           pos: Optional[torch.Tensor] = None, pos_table: Optional[torch.Tensor] = None) -> None:
     _need(ids, torch.int32, "embed ids")

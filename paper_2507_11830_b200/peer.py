@@ -3,7 +3,8 @@
 Each rank owns, at addresses every peer knows:
   recv  bf16 [max_tokens, W]           seq->head receive (QKV GEMM epilogue stores here)
   back  bf16 [P * rows_max, hq_l * d]  head->seq receive ([P][rows][w], O-proj A operand)
-  flags int32 [2, P]                   completion flags (fwd, back), one slot per sender
+  flags int32 [4, P]                   completion flags (fwd, back, tp-attn, tp-mlp)
+  part  f32 [2, max_tokens, h]         TP partials (O-proj, down-proj) read by every peer
 
 Device tables of the P peers' addresses feed the kernels (sp_gemm_bf16_to_peers,
 sp_peer_scatter_rows, sp_peer_signal).  In-process ranks (LoopbackGroup) use
@@ -28,7 +29,7 @@ def _align(n: int, a: int = 256) -> int:
 
 class PeerLinks:
     def __init__(self, group: DeviceGroup, max_tokens: int, width_qkv: int, width_back: int,
-                 device: torch.device):
+                 hidden: int, device: torch.device):
         P = group.world_size
         self.P = P
         self.max_tokens = max_tokens
@@ -37,13 +38,17 @@ class PeerLinks:
         self.w_back = width_back
         n_recv = max_tokens * width_qkv * 2
         n_back = P * self.rows_max * width_back * 2
-        n_flag = 2 * P * 4
+        self.hidden = hidden
+        n_part = 2 * max_tokens * hidden * 4
+        n_flag = 4 * P * 4
         self.off_recv, self.off_back = 0, _align(n_recv)
-        self.off_flags = self.off_back + _align(n_back)
+        self.off_part = self.off_back + _align(n_back)
+        self.off_flags = self.off_part + _align(n_part)
         total = self.off_flags + _align(n_flag)
         self.recv: Dict[int, torch.Tensor] = {}
         self.back: Dict[int, torch.Tensor] = {}
         self.flags: Dict[int, torch.Tensor] = {}
+        self.part: Dict[int, list] = {}
         bases: List[int] = [0] * P
         if isinstance(group, LoopbackGroup):
             self._bufs = {}
@@ -70,8 +75,10 @@ class PeerLinks:
 
         self.recv_ptrs = table(self.off_recv)
         self.back_ptrs = table(self.off_back)
+        self.part_ptrs = [table(self.off_part), table(self.off_part + max_tokens * hidden * 4)]
         self.fwd_flag_ptrs = table(self.off_flags)
         self.back_flag_ptrs = table(self.off_flags + P * 4)
+        self.tp_flag_ptrs = [table(self.off_flags + 2 * P * 4), table(self.off_flags + 3 * P * 4)]
 
     def _views(self, r: int, buf: torch.Tensor) -> None:
         P = self.P
@@ -80,7 +87,13 @@ class PeerLinks:
         nb = P * self.rows_max * self.w_back
         self.back[r] = buf[self.off_back:self.off_back + nb * 2].view(torch.bfloat16) \
             .view(P * self.rows_max, self.w_back)
-        self.flags[r] = buf[self.off_flags:self.off_flags + 2 * P * 4].view(torch.int32).view(2, P)
+        self.flags[r] = buf[self.off_flags:self.off_flags + 4 * P * 4].view(torch.int32).view(4, P)
+        npart = self.max_tokens * self.hidden
+        self.part.setdefault(r, [None, None])
+        for i in range(2):
+            lo = self.off_part + i * npart * 4
+            self.part[r][i] = buf[lo:lo + npart * 4].view(torch.float32).view(self.max_tokens,
+                                                                              self.hidden)
 
 
 def fused_a2a_enabled(group: DeviceGroup) -> bool:

@@ -423,3 +423,28 @@ def test_fused_peer_all_to_all_matches_collective_path(c1_kv4, p, monkeypatch):
     for a, b in zip(res["1"][0], res["0"][0]):
         assert torch.equal(a, b)
     assert res["1"][1] == res["0"][1]
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_fused_tp_allreduce_matches_collective_path(c1_kv4, p, monkeypatch):
+    """TP with the one-shot all-reduce fused into the add+RMSNorm kernel (partials
+    summed from peer buffers in ascending rank order) is bit-identical to the
+    collective path, prefill and graph-replayed decode, with the same ledger."""
+    prompts = [c1_prompts()[i][:50] for i in (2, 3)]
+    res = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("SP_FUSED_A2A", fused)
+        eng = make(c1_kv4, p)
+        seqs = [eng.new_sequence(i, capacity=100) for i in range(2)]
+        lg, rec = eng.step(Batch(BatchKind.PREFILL, [BatchItem(s, q) for s, q in zip(seqs, prompts)]),
+                           mode=ParallelMode.TP, span_logits=True)
+        out, recs = [x.cpu() for x in lg], [rec.comm]
+        for step in range(3):
+            lg, rec = eng.step(Batch(BatchKind.DECODE, [BatchItem(s, [9 + step]) for s in seqs]),
+                               mode=ParallelMode.TP)
+            out += [x.cpu() for x in lg]
+            recs.append(rec.comm)
+        res[fused] = (out, recs)
+    for a, b in zip(res["1"][0], res["0"][0]):
+        assert torch.equal(a, b)
+    assert res["1"][1] == res["0"][1]
