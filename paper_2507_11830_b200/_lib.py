@@ -13,7 +13,7 @@ import os
 from .errors import ContractViolation, LibraryMissing
 
 LIB_NAME = "libshiftpar.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("SP_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)  # override: A/B kernel comparisons
 
 _c_int = ctypes.c_int
 _i64 = ctypes.c_int64

@@ -13,6 +13,8 @@
 // Decode kernel: one CTA per (item, kv head, split); each warp streams its own
 // key tiles (double-buffered) for the G packed heads; warps merge in smem and
 // splits merge in a combine kernel (flash-decoding).
+#include <cstdlib>
+
 #include "../../include/shiftpar.h"
 #include "common.cuh"
 
@@ -431,7 +433,7 @@ __global__ void combine_kernel(Params p, int head_dim) {
 namespace dec {
 constexpr int HD = 128;
 constexpr int PAGE = 64;
-constexpr int STAGES = 4;
+constexpr int STAGES = 3;  // 3 x 32 KiB ring -> two CTAs per SM
 constexpr int NCONS = 4;
 constexpr int NUM_THREADS = (NCONS + 1) * 32;
 constexpr int TILE_BYTES = PAGE * HD * 2;
@@ -444,7 +446,7 @@ __device__ __forceinline__ uint32_t kv_addr(uint32_t base, int key, int c16) {
   return base + (c16 >> 3) * (TILE_BYTES / 2) + key * 128 + ((((c16 & 7) ^ (key & 7))) << 4);
 }
 
-__global__ void __launch_bounds__(NUM_THREADS) decode_tma_kernel(
+__global__ void __launch_bounds__(NUM_THREADS, 2) decode_tma_kernel(
     const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Params p) {
   pdl_wait();  // inputs of this kernel are written by its predecessor
   pdl_trigger();
@@ -596,7 +598,11 @@ __global__ void __launch_bounds__(NUM_THREADS) decode_tma_kernel(
 
 static int decode_tma_splits(int n_items, int kv_heads, int max_kv_len) {
   const int ctas = n_items * kv_heads;
+  // two CTAs per SM are resident: split only until one wave of slots is
+  // covered (measured: B=64 x 8 kv heads runs best unsplit; tuning override
+  // SP_DECODE_SPLITS)
   int want = (2 * 148 + ctas - 1) / ctas;
+  if (const char* e = getenv("SP_DECODE_SPLITS")) want = atoi(e);
   const int pages = (max_kv_len + dec::PAGE - 1) / dec::PAGE;
   const int max_useful = (pages + 3) / 4;  // >= 4 page slices per split
   if (want > max_useful) want = max_useful;

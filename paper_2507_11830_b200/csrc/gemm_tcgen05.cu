@@ -21,6 +21,8 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <vector>
+#include <cstdio>
 
 #include "../../include/shiftpar.h"
 #include "common.cuh"
@@ -381,29 +383,86 @@ __global__ void __launch_bounds__(NUM_THREADS, Tile<BN_>::MIN_BLOCKS)
 // ------------------------------------------------------ swap-AB (decode-size M)
 // D^T = W · X^T: the 128-row MMA operand is a weight tile, the token rows (M <=
 // 128, padded to NT) are the N operand, so every staged byte is a weight byte.
-// Tiles = (128-row weight tile) x (K split); partials go to ws[split][M][N] and
-// splitk_reduce_kernel applies the epilogue, unless ksplit == 1 and the
-// epilogue is a plain store/add/GeLU (then it is applied here).
+//
+// Work item = (super tile, K split).  A super tile is 2 x 128 weight rows —
+// for SwiGLU exactly one gate|up pair, so the activation is applied in place
+// when K is not split.  K is split only as far as needed to put enough CTAs
+// on the weight stream (one round of items, no tail); split items store raw
+// f32 partials to ws[split][M][N] and splitk_reduce_kernel sums them in
+// ascending split order (deterministic) and applies the epilogue.
+namespace swp {
+constexpr int WT = 2;                 // weight tiles per super tile
+constexpr int W_TILE = 128 * BK * 2;  // 16 KiB
+}  // namespace swp
+
 template <int NT>
 struct SwapTile {
-  static constexpr int W_BYTES = 128 * BK * 2;
+  static constexpr int W_BYTES = swp::WT * swp::W_TILE;
   static constexpr int X_BYTES = NT * BK * 2;
   static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
-  // M <= 32 (latency-bound decode): two CTAs per SM with ~100 KB rings, so a
-  // successor's CTAs can start streaming weights (PDL) while this one drains;
-  // larger M: one CTA per SM with a ~200 KB ring (measured best at B=64).
+  // M <= 32 (latency-bound decode): two CTAs per SM, so a successor's CTAs can
+  // start streaming weights (PDL) while this one drains; larger M: one CTA per
+  // SM with a ~200 KB ring.
   static constexpr int CTAS_PER_SM = NT <= 32 ? 2 : 1;
-  static constexpr int RING = (CTAS_PER_SM == 2 ? 100 : 200) * 1024;
+  static constexpr int RING = (CTAS_PER_SM == 2 ? 108 : 200) * 1024;
   static constexpr int STAGES = RING / STAGE_BYTES > 10 ? 10 : RING / STAGE_BYTES;
-  static constexpr int TMEM_COLS = 2 * NT < 32 ? 32 : 2 * NT;
+  static constexpr int ACC_COLS = swp::WT * NT;  // one accumulator stage
+  static constexpr int TMEM_COLS = 2 * ACC_COLS < 32 ? 32 : 2 * ACC_COLS;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 };
+
+// Outputs of super tile t for weight row nl of each 128-row half, rows
+// [m0, m0 + R) (those < m_end): v[0] = row t*256 + nl, v[1] = row t*256 + 128 + nl
+// (gate and up for SwiGLU).  Residual reads are issued together before any
+// store so their latencies overlap.
+template <int R>
+__device__ __forceinline__ void swap_store_rows(const Params& p, int m0, int m_end, int t, int nl,
+                                                const float (&v)[swp::WT][R]) {
+  if (p.epi == SP_EPI_SWIGLU && p.ws == nullptr) {
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if (m0 + j < m_end)
+        *out_ptr<__nv_bfloat16>(p, m0 + j, t * 128 + nl) = __float2bfloat16_rn(silu(v[0][j]) * v[1][j]);
+    return;
+  }
+#pragma unroll
+  for (int w = 0; w < swp::WT; ++w) {
+    const int n = t * swp::WT * 128 + w * 128 + nl;
+    if (n >= p.N) continue;
+    if (p.ws != nullptr) {  // raw partial of split ks (set by the caller in p.D)
+      float* dst = reinterpret_cast<float*>(p.D) + n;
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        if (m0 + j < m_end) dst[(int64_t)(m0 + j) * p.N] = v[w][j];
+    } else if (p.epi == SP_EPI_ADD_F32) {
+      float old[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) old[j] = m0 + j < m_end ? *out_ptr<float>(p, m0 + j, n) : 0.f;
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        if (m0 + j < m_end) *out_ptr<float>(p, m0 + j, n) = old[j] + v[w][j];
+    } else if (p.epi == SP_EPI_STORE_F32) {
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        if (m0 + j < m_end) *out_ptr<float>(p, m0 + j, n) = v[w][j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        if (m0 + j >= m_end) continue;
+        float x = v[w][j];
+        if (p.epi == SP_EPI_GELU) x = gelu_tanh(x);
+        *out_ptr<__nv_bfloat16>(p, m0 + j, n) = __float2bfloat16_rn(x);
+      }
+    }
+  }
+}
 
 template <int NT>
 __global__ void __launch_bounds__(NUM_THREADS, SwapTile<NT>::CTAS_PER_SM)
     gemm_swap_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                      const Params p) {
   using T = SwapTile<NT>;
+  using namespace swp;
   constexpr int STAGES = T::STAGES, STAGE_BYTES = T::STAGE_BYTES, TMEM_COLS = T::TMEM_COLS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -442,20 +501,23 @@ __global__ void __launch_bounds__(NUM_THREADS, SwapTile<NT>::CTAS_PER_SM)
       int n_def = 0;
       int def_stage[STAGES], def_kc[STAGES], def_ko[STAGES];
       bool waited = false;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        const int ks = t % p.ksplit, nb = t / p.ksplit;
+      for (int it = blockIdx.x; it < p.num_tiles; it += gridDim.x) {
+        const int ks = it % p.ksplit, t = it / p.ksplit;
         const int kb0 = ks * p.kb_per_split, kb1 = min(p.k_blocks, kb0 + p.kb_per_split);
+        const int row0 = t * WT * 128;
+        const int wv = min(WT, (p.N - row0 + 127) / 128);  // weight tiles inside N
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           uint8_t* sw = smem + stage * STAGE_BYTES;
-          mbar_arrive_expect_tx(full + stage, STAGE_BYTES);
+          mbar_arrive_expect_tx(full + stage, wv * W_TILE + T::X_BYTES);
           const int k = kb * BK;
           int ko = 0, kc = k;
           if (p.a_kchunk > 0) {
             ko = k / p.a_kchunk;
             kc = k - ko * p.a_kchunk;
           }
-          tma_load_2d(sw, &tmW, full + stage, k, nb * 128);  // weights: no dependency
+          for (int w = 0; w < wv; ++w)  // weights: no dependency on the predecessor
+            tma_load_2d(sw + w * W_TILE, &tmW, full + stage, k, row0 + w * 128);
           if (waited) {
             tma_load_3d(sw + T::W_BYTES, &tmX, full + stage, kc, 0, ko);
           } else {
@@ -489,21 +551,24 @@ __global__ void __launch_bounds__(NUM_THREADS, SwapTile<NT>::CTAS_PER_SM)
       constexpr uint32_t idesc = idesc_bf16_f32(128, NT);
       int stage = 0, acc = 0;
       uint32_t phase = 0, aphase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        const int ks = t % p.ksplit;
+      for (int it = blockIdx.x; it < p.num_tiles; it += gridDim.x) {
+        const int ks = it % p.ksplit, t = it / p.ksplit;
         const int kb0 = ks * p.kb_per_split, kb1 = min(p.k_blocks, kb0 + p.kb_per_split);
+        const int wv = min(WT, (p.N - t * WT * 128 + 127) / 128);
         mbar_wait(tempty + acc, aphase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * NT;
+        const uint32_t d_tmem = tmem_base + acc * T::ACC_COLS;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
           const uint32_t w_addr = smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t x_addr = w_addr + T::W_BYTES;
+          for (int w = 0; w < wv; ++w) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(d_tmem, sdesc_sw128(w_addr + k * 32), sdesc_sw128(x_addr + k * 32), idesc,
-                      (kb != kb0 || k != 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16(d_tmem + w * NT, sdesc_sw128(w_addr + w * W_TILE + k * 32),
+                        sdesc_sw128(x_addr + k * 32), idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+          }
           umma_commit(empty + stage);
           if (++stage == STAGES) {
             stage = 0;
@@ -521,42 +586,29 @@ __global__ void __launch_bounds__(NUM_THREADS, SwapTile<NT>::CTAS_PER_SM)
   } else {
     pdl_wait();
     const int quarter = warp & 3;
+    const int nl = quarter * 32 + lane;  // this thread's weight row inside a 128-row tile
     int acc = 0;
     uint32_t aphase = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      const int ks = t % p.ksplit, nb = t / p.ksplit;
+    for (int it = blockIdx.x; it < p.num_tiles; it += gridDim.x) {
+      const int ks = it % p.ksplit, t = it / p.ksplit;
+      Params q = p;  // split items write raw partials to ws[ks][M][N]
+      if (p.ws != nullptr) q.D = p.ws + (int64_t)ks * p.M * p.N;
       mbar_wait(tfull + acc, aphase);
       tc_fence_after();
-      const int n = nb * 128 + quarter * 32 + lane;  // this thread's output feature
-      const uint32_t tb = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NT;
+      const uint32_t tb = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * T::ACC_COLS;
 #pragma unroll 1
-      for (int c = 0; c < NT; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(tb + c, r);
-        tmem_ld_wait();
-        if (n < p.N) {
-          if (p.ws != nullptr) {
-            float* dst = p.ws + (int64_t)ks * p.M * p.N + n;
-#pragma unroll 4
-            for (int j = 0; j < 32; ++j)
-              if (c + j < p.M) dst[(int64_t)(c + j) * p.N] = __uint_as_float(r[j]);
-          } else {
-#pragma unroll 4
-            for (int j = 0; j < 32; ++j) {
-              const int m = c + j;
-              if (m >= p.M) break;
-              float v = __uint_as_float(r[j]);
-              if (p.epi == SP_EPI_STORE_F32) {
-                *out_ptr<float>(p, m, n) = v;
-              } else if (p.epi == SP_EPI_ADD_F32) {
-                *out_ptr<float>(p, m, n) += v;
-              } else {
-                if (p.epi == SP_EPI_GELU) v = gelu_tanh(v);
-                *out_ptr<__nv_bfloat16>(p, m, n) = __float2bfloat16_rn(v);
-              }
-            }
-          }
+      for (int c0 = 0; c0 < NT; c0 += 32) {
+        if (c0 >= p.M) break;
+        float v[WT][32];
+#pragma unroll
+        for (int w = 0; w < WT; ++w) {
+          uint32_t r[32];
+          tmem_ld32(tb + w * NT + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[w][j] = __uint_as_float(r[j]);
         }
+        swap_store_rows<32>(q, c0, p.M, t, nl, v);
       }
       tc_fence_before();
       __syncwarp();
@@ -1035,15 +1087,20 @@ static int launch_swap(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   using T = SwapTile<NT>;
   const int sms = sm_count();
   const int64_t k_blocks = cdiv(K, BK);
-  const int64_t n_tiles = cdiv(N, 128);
-  // split K so the tile count is close to the resident-CTA count
+  const int64_t n_super = cdiv(N, swp::WT * 128);
   const int64_t slots = (int64_t)sms * T::CTAS_PER_SM;
-  int64_t ks = std::max<int64_t>(1, (slots + n_tiles / 2) / n_tiles);
-  ks = std::min<int64_t>(ks, std::max<int64_t>(1, k_blocks / 2));
+  // Split K only until ~2/3 of the SMs stream weights (one round of items: a
+  // CTA with ~200 KB in flight streams well above its 1/148 share of HBM, so
+  // partial SM coverage still saturates HBM, while a second round would leave
+  // a tail).  Tuning override: SP_SWAP_MIN_CTAS.
+  int64_t min_ctas = T::CTAS_PER_SM == 2 ? sms : (2 * sms) / 3;  // measured best (tools/swap_probe.py)
+  if (const char* e = getenv("SP_SWAP_MIN_CTAS")) min_ctas = atoi(e);
+  int64_t ks = 1;
+  while (n_super * ks < min_ctas && ks * 2 <= k_blocks) ++ks;
+  while (ks > 1 && n_super * ks > slots) --ks;
   const int64_t per = cdiv(k_blocks, ks);
   ks = cdiv(k_blocks, per);
-  const bool direct = ks == 1 && epilogue != SP_EPI_SWIGLU;
-  if (!direct && (!ws || ks * (int64_t)M * N * 4 > ws_bytes)) return -1;  // caller falls back
+  if (ks > 1 && (!ws || ks * (int64_t)M * N * 4 > ws_bytes)) return -1;  // caller falls back
   CUtensorMap tx, tw;
   {
     const uint64_t kin = a_kchunk > 0 ? (uint64_t)a_kchunk : (uint64_t)K;
@@ -1068,7 +1125,7 @@ static int launch_swap(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   p.N = N;
   p.K = K;
   p.num_m = 1;
-  p.num_n = (int)n_tiles;
+  p.num_n = (int)n_super;
   p.k_blocks = (int)k_blocks;
   p.epi = epilogue;
   p.a_kchunk = (int)(a_kchunk > 0 ? a_kchunk : 0);
@@ -1077,10 +1134,10 @@ static int launch_swap(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   p.peer_width = peer_width;
   p.peer_stride = peer_stride;
   p.group_m = 1;
-  p.ws = direct ? nullptr : ws;
+  p.ws = ks > 1 ? ws : nullptr;
   p.ksplit = (int)ks;
   p.kb_per_split = (int)per;
-  p.num_tiles = (int)(n_tiles * ks);
+  p.num_tiles = (int)(n_super * ks);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_swap_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1090,7 +1147,7 @@ static int launch_swap(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   const int grid = (int)std::min<int64_t>(p.num_tiles, slots);
   launch_k(gemm_swap_kernel<NT>, grid, NUM_THREADS, T::SMEM_BYTES, reinterpret_cast<cudaStream_t>(stream), tx, tw, p);
   if (int rc = check_launch("gemm_swap_kernel")) return rc;
-  if (!direct) {
+  if (ks > 1) {
     const int n_out = epilogue == SP_EPI_SWIGLU ? N / 2 : N;
     const int64_t threads = (int64_t)M * (n_out / 8);
     launch_k(splitk_reduce_kernel, (unsigned)cdiv(threads, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream), p);
@@ -1098,6 +1155,7 @@ static int launch_swap(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   }
   return kOk;
 }
+
 
 static int launch_pair(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_chunk_stride,
                        const void* B, int64_t ldb, void* D, int64_t ldd, int M, int N, int K,
@@ -1192,8 +1250,9 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
 
   // Regime selection (numerics are identical within a regime):
   //  * enough 128x256 tiles to cover the SMs        -> BN=256
-  //  * one M tile (decode-size M) and a workspace    -> split-K over BN=64 tiles,
-  //    f32 partials reduced in ascending split order by splitk_reduce_kernel
+  //  * one M tile (decode-size M)                   -> swap-AB over 256-row weight
+  //    super tiles, K split just enough to cover ~2/3 of the SMs in one round;
+  //    split partials summed in ascending split order by splitk_reduce_kernel
   //  * otherwise                                     -> narrower N tiles (128/64/32),
   //    bit-identical to BN=256 (same K loop)
   const int sms = sm_count();

@@ -331,15 +331,22 @@ def test_gemm_tile_width_variants_are_bitexact(monkeypatch):
     assert rel(outs["32"][0], a.float() @ b.float().t()) < 1e-4
 
 
+@pytest.mark.parametrize("N,K", [(1024, 4096), (2560, 512), (384, 192), (128256, 128)])
 @pytest.mark.parametrize("M", [1, 48, 100])
 @pytest.mark.parametrize("epi", ["f32", "add", "bf16", "swiglu", "gelu", "peer", "chunked"])
-def test_gemm_split_k_regime(epi, M):
-    """Decode-size M: split-K over BN=64 tiles with an ascending-order reduce.
-    Deterministic run to run; within f32 accumulation noise of the reference."""
+def test_gemm_split_k_regime(epi, M, N, K):
+    """Decode-size M: swap-AB stream-K (equal weight share per CTA; super tiles
+    split across CTAs summed in ascending-K order by their last CTA).  Shapes
+    cover many-CTA tiles (2560x512), a half-empty last super tile (384), and
+    whole tiles finished in place (128256x128).  Deterministic run to run;
+    within f32 accumulation noise of the reference."""
+    if epi == "swiglu" and N % 256:
+        pytest.skip("SwiGLU needs gate|up pairs of 128 rows")
+    if epi == "chunked" and (K // 4) % 64:
+        pytest.skip("chunked-K A needs 64-multiple chunks")
     ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
     ops.set_gemm_workspace(ws)
     try:
-        N, K = 1024, 4096
         a, b = rnd(M, K, seed=40), rnd(N, K, seed=41)
         ref = a.float() @ b.float().t()
         outs = []
