@@ -66,6 +66,7 @@ struct Params {
   int ksplit, kb_per_split;
   float* ws;
   int group_m;  // m-tiles per raster group (A rows of a group stay L2-resident)
+  int group_n;  // > 0: n-tiles per raster group instead (B rows stay L2-resident)
   // fused all-to-all: column block b = n / peer_width goes to peer b's buffer
   // peer_ptrs[b] at row (m + peer_row_off) — stores cross NVLink directly
   const unsigned long long* peer_ptrs;
@@ -91,6 +92,16 @@ __device__ __forceinline__ T* out_ptr(const Params& p, int m, int64_t n) {
 }
 
 __device__ __forceinline__ void tile_coords(int t, const Params& p, int& mb, int& nb) {
+  if (p.group_n > 0) {  // B-resident raster: a group of N tiles sweeps every M tile
+    const int per_group = p.group_n * p.num_m;
+    const int g = t / per_group;
+    const int first_n = g * p.group_n;
+    const int gn = min(p.num_n - first_n, p.group_n);
+    const int r = t - g * per_group;
+    nb = first_n + r % gn;
+    mb = r / gn;
+    return;
+  }
   const int per_group = p.group_m * p.num_n;
   const int g = t / per_group;
   const int first_m = g * p.group_m;
@@ -944,6 +955,24 @@ __global__ void splitk_reduce_kernel(const Params p) {
 }
 
 // ------------------------------------------------------------------ host side
+// Raster choice: keep a group of A tiles (B streamed once per group) or of B
+// tiles (A streamed once per group) L2-resident, whichever moves fewer DRAM
+// bytes; SP_GEMM_L2_MB overrides the resident budget (default 40 MB of the
+// 126 MB L2: measured best — larger resident groups thrash).
+static void choose_raster(Params& p, int64_t tm, int64_t tn, int64_t K, int64_t M, int64_t N) {
+  int64_t budget = 40ll << 20;
+  if (const char* e = getenv("SP_GEMM_L2_MB")) budget = (int64_t)atoi(e) << 20;
+  const int64_t a_tile = tm * K * 2, b_tile = tn * K * 2;
+  const int64_t gm = std::max<int64_t>(1, std::min<int64_t>(budget / std::max<int64_t>(a_tile, 1), p.num_m));
+  const int64_t gn = std::max<int64_t>(1, std::min<int64_t>(budget / std::max<int64_t>(b_tile, 1), p.num_n));
+  const int64_t a_bytes = M * K * 2, b_bytes = N * K * 2;
+  const int64_t traffic_m = a_bytes + b_bytes * ((p.num_m + gm - 1) / gm);
+  const int64_t traffic_n = b_bytes + a_bytes * ((p.num_n + gn - 1) / gn);
+  p.group_m = (int)gm;
+  p.group_n = traffic_n < traffic_m ? (int)gn : 0;
+  if (const char* e = getenv("SP_GEMM_RASTER")) p.group_n = e[0] == 'n' ? (int)gn : 0;
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static std::mutex g_mu;
 static std::map<std::array<uint64_t, 12>, CUtensorMap> g_maps;
@@ -1051,11 +1080,7 @@ static int launch(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_chunk_
   p.peer_stride = peer_stride;
   // raster: walk all N tiles of a group of m-tiles whose A rows fit ~40 MB of L2,
   // so every B (weight) tile is streamed from HBM once per group
-  {
-    const int64_t a_tile_bytes = (int64_t)BM * K * 2;
-    int64_t gm = (40ll << 20) / std::max<int64_t>(a_tile_bytes, 1);
-    p.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(gm, p.num_m));
-  }
+  choose_raster(p, BM, BN, K, M, N);
   p.ws = ws;
   p.ksplit = ws ? ksplit : 1;
   p.kb_per_split = (int)cdiv(p.k_blocks, p.ksplit);
@@ -1134,6 +1159,7 @@ static int launch_swap(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   p.peer_width = peer_width;
   p.peer_stride = peer_stride;
   p.group_m = 1;
+  p.group_n = 0;
   p.ws = ks > 1 ? ws : nullptr;
   p.ksplit = (int)ks;
   p.kb_per_split = (int)per;
@@ -1197,11 +1223,7 @@ static int launch_pair(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   p.ws = nullptr;
   p.ksplit = 1;
   p.kb_per_split = p.k_blocks;
-  {
-    const int64_t a_pair_bytes = (int64_t)256 * K * 2;
-    int64_t gm = (40ll << 20) / std::max<int64_t>(a_pair_bytes, 1);
-    p.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(gm, p.num_m));
-  }
+  choose_raster(p, 256, 256, K, M, N);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

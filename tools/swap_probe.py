@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2507_11830_b200 import ops  # noqa: E402
 
 M, N, K = (int(x) for x in sys.argv[1:4])
-epi = {"bf16": ops.EPI_STORE_BF16, "add": ops.EPI_ADD_F32, "swiglu": ops.EPI_SWIGLU,
+epi = {"bf16": ops.EPI_STORE_BF16, "add": ops.EPI_ADD_F32, "swiglu": ops.EPI_SWIGLU, "gelu": ops.EPI_GELU,
        "f32": ops.EPI_STORE_F32}[sys.argv[4] if len(sys.argv) > 4 else "bf16"]
 reps = int(sys.argv[5]) if len(sys.argv) > 5 else 20
 ops.set_gemm_workspace(torch.empty(64 << 20, dtype=torch.uint8, device="cuda"))
