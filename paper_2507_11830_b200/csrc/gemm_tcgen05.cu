@@ -607,19 +607,21 @@ __global__ void __launch_bounds__(NUM_THREADS, SwapTile<NT>::CTAS_PER_SM)
       mbar_wait(tfull + acc, aphase);
       tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * T::ACC_COLS;
+      // 8 token rows per step, rolled: the epilogue runs once per item, so
+      // compact code matters more than unrolling (a fully unrolled version
+      // stalled on instruction fetch)
 #pragma unroll 1
-      for (int c0 = 0; c0 < NT; c0 += 32) {
-        if (c0 >= p.M) break;
-        float v[WT][32];
+      for (int c0 = 0; c0 < p.M; c0 += 8) {
+        float v[WT][8];
 #pragma unroll
         for (int w = 0; w < WT; ++w) {
-          uint32_t r[32];
-          tmem_ld32(tb + w * NT + c0, r);
+          uint32_t r[8];
+          tmem_ld8(tb + w * NT + c0, r);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[w][j] = __uint_as_float(r[j]);
+          for (int j = 0; j < 8; ++j) v[w][j] = __uint_as_float(r[j]);
         }
-        swap_store_rows<32>(q, c0, p.M, t, nl, v);
+        swap_store_rows<8>(q, c0, p.M, t, nl, v);
       }
       tc_fence_before();
       __syncwarp();
