@@ -207,11 +207,19 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
+    # SP_BENCH_BACKEND=gloo (test only): several ranks share the GPUs present,
+    # collectives staged through host memory — exercises the N>1 plumbing on a
+    # 1-GPU box; measured runs use NCCL, one rank per GPU
+    backend = os.environ.get("SP_BENCH_BACKEND", "nccl")
+    dev_idx = local % torch.cuda.device_count() if backend == "gloo" else local
+    torch.cuda.set_device(dev_idx)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ops.device_check()
     pk = peaks()
 
@@ -252,7 +260,7 @@ def run_ours(args):
         prefill()
     # ---------------- timed region: device-resident inputs, CUDA events
     sync_barrier()
-    clocks = Clocks(local)
+    clocks = Clocks(dev_idx)
     clocks.start()
     launches0 = ops.kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -378,7 +386,7 @@ def run_ours(args):
         kv_bytes = dec_b * (args.decode_ctx + 20) * cfg.n_layers * 2 * (cfg.kv_heads // world) * cfg.head_dim * 2
         step_bytes = wbytes // world + kv_bytes
         decode = {"tpot_ms": round(tpot, 4), "tpot_ms_eager": round(tpot_eager, 4),
-                  "cuda_graphs": True, "batch": dec_b, "ctx": args.decode_ctx, "mode": "tp",
+                  "cuda_graphs": not getattr(group, "_stage", False), "batch": dec_b, "ctx": args.decode_ctx, "mode": "tp",
                   "hbm_roofline_tpot_ms": round(step_bytes / (pk["hbm_gbs"] * 1e9) * 1e3, 4),
                   "frac_of_hbm_roofline": round(step_bytes / (pk["hbm_gbs"] * 1e9) * 1e3 / tpot, 4),
                   "attn_decode": {"achieved_gbs": round(ad_b / (ad_ms / 1e3) / 1e9, 1) if ad_ms else None,

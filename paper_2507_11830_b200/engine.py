@@ -303,6 +303,7 @@ class Engine:
         cut = cut_full if use_swiftkv else None
         graph_key = None
         if (self.cuda_graphs and cut is None and not span_logits
+                and not getattr(self.group, "_stage", False)  # host-staged collectives
                 and all(len(it.tokens) == 1 for it in batch.items)):
             graph_key = (mode, len(batch.items), self._bt_width_cap(batch))
         shape = self.pass_shape(batch, span_logits) if graph_key else None

@@ -153,19 +153,36 @@ class NcclGroup(DeviceGroup):
             torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
             else torch.device("cpu"))
         self._dist = dist
+        # gloo cannot move CUDA tensors: stage through host memory (used to run
+        # several ranks on ONE GPU in tests; B200 runs use NCCL directly)
+        self._stage = dist.get_backend() == "gloo" and self.device.type == "cuda"
 
     def all_to_all(self, send, recv, in_splits, out_splits, row_bytes) -> None:
         me = self.rank
         if self.world_size > 1:
-            self._dist.all_to_all_single(recv[me], send[me], output_split_sizes=out_splits[me],
-                                         input_split_sizes=in_splits[me])
+            if self._stage:
+                s = send[me].cpu()
+                r = torch.empty(recv[me].shape, dtype=s.dtype)
+                if s.dtype == torch.bfloat16:  # pure data movement: move the bytes
+                    s, r = s.view(torch.uint8), r.view(torch.uint8)
+                self._dist.all_to_all_single(r, s, output_split_sizes=out_splits[me],
+                                             input_split_sizes=in_splits[me])
+                recv[me].copy_(r.view(recv[me].dtype))
+            else:
+                self._dist.all_to_all_single(recv[me], send[me], output_split_sizes=out_splits[me],
+                                             input_split_sizes=in_splits[me])
         self._charge_a2a(in_splits, row_bytes)
 
     def all_reduce_sum(self, parts):
         me, p = self.rank, self.world_size
         t = parts[me]
         if p > 1:
-            self._dist.all_reduce(t)
+            if self._stage:
+                h = t.cpu()
+                self._dist.all_reduce(h)
+                t.copy_(h)
+            else:
+                self._dist.all_reduce(t)
         self.charge("all_reduce", [2.0 * (p - 1) / p * t.numel() * t.element_size()] * p)
         return {me: t}
 
@@ -179,8 +196,13 @@ class NcclGroup(DeviceGroup):
         else:
             pad = torch.zeros((mx, width), dtype=t.dtype, device=t.device)
             pad[:counts[me]].copy_(t[:counts[me]])
-            buf = torch.empty((p * mx, width), dtype=t.dtype, device=t.device)
-            self._dist.all_gather_into_tensor(buf, pad)
+            if self._stage:
+                chunks = [torch.empty((mx, width), dtype=t.dtype) for _ in range(p)]
+                self._dist.all_gather(chunks, pad.cpu())
+                buf = torch.cat(chunks, dim=0).to(t.device)
+            else:
+                buf = torch.empty((p * mx, width), dtype=t.dtype, device=t.device)
+                self._dist.all_gather_into_tensor(buf, pad)
             full = torch.cat([buf[r * mx:r * mx + counts[r]] for r in range(p)], dim=0)
         nbytes = sum(counts) * width * t.element_size()
         self.charge("all_gather", [(p - 1) / p * nbytes] * p)

@@ -1,0 +1,119 @@
+"""The N>1 engine path with one process per rank (the torchrun/NCCL layout of
+bench.py --gpus N), run as 2 processes sharing the one available B200.
+
+NCCL refuses two ranks on one GPU, so the NcclGroup here runs over gloo and
+stages its collectives through host memory; everything else — the SPMD
+metadata every rank builds, its own head shard of the paged cache, its own
+token shard, the split tables of the SP all-to-alls (uneven and empty
+shards), the TP all-reduce and the logits all-gather — is the code path the
+8-GPU run takes.  The result must be bit-identical to the in-process
+LoopbackGroup(2) engine (for two ranks every collective sum is a single
+commutative add, so no reduction-order freedom remains).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import c1_prompts, device_weights
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _schedule():
+    """C1 prompts (SP prefill), then decode passes alternating TP / SP, the last
+    SP decode with ONE request (token shards [1, 0]: an empty shard)."""
+    prompts = c1_prompts()[:3]
+    return prompts
+
+
+def _run(engine_factory):
+    from paper_2507_11830_b200 import Batch, BatchItem, BatchKind, ParallelMode
+    eng = engine_factory()
+    prompts = _schedule()
+    seqs = [eng.new_sequence(i, capacity=256) for i in range(len(prompts))]
+    out = []
+    lg, _ = eng.step(Batch(BatchKind.PREFILL, [BatchItem(s, p) for s, p in zip(seqs, prompts)]),
+                     mode=ParallelMode.SP)
+    out.append(np.stack([x.cpu().numpy() for x in lg]))
+    toks = [int(np.argmax(r)) for r in out[-1]]
+    for mode in (ParallelMode.TP, ParallelMode.SP, ParallelMode.TP):
+        lg, _ = eng.step(Batch(BatchKind.DECODE, [BatchItem(s, [t]) for s, t in zip(seqs, toks)]),
+                         mode=mode)
+        out.append(np.stack([x.cpu().numpy() for x in lg]))
+        toks = [int(np.argmax(r)) for r in out[-1]]
+    lg, _ = eng.step(Batch(BatchKind.DECODE, [BatchItem(seqs[0], [toks[0]])]), mode=ParallelMode.SP)
+    out.append(np.stack([x.cpu().numpy() for x in lg]))
+    fp = seqs[0].cache.fingerprint()
+    return out, [s.cache.write_counter for s in seqs], fp
+
+
+def _worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.model import init_weights_llama, llama_tiny_config
+        from paper_2507_11830_b200 import Engine, NcclGroup, ShiftPolicy
+        ow = init_weights_llama(llama_tiny_config(max_seq=512), seed=0)
+
+        def factory():
+            # cuda_graphs off: graph capture cannot contain host-staged collectives
+            return Engine(device_weights(ow, world), NcclGroup(), ShiftPolicy.fixed_tp(),
+                          cuda_graphs=False)
+
+        out, wc, fp = _run(factory)
+        q.put((rank, ([o.tolist() for o in out], wc, repr(fp))))
+    except Exception as e:  # surface worker failures in the parent
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_process_engine_matches_loopback():
+    import torch.multiprocessing as mp
+    from oracle.model import init_weights_llama, llama_tiny_config
+    from paper_2507_11830_b200 import Engine, LoopbackGroup, ShiftPolicy
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    for r in range(world):
+        assert not isinstance(res[r], str), f"rank {r} failed: {res[r]}"
+        assert procs[r].exitcode == 0
+
+    ow = init_weights_llama(llama_tiny_config(max_seq=512), seed=0)
+    want, want_wc, want_fp = _run(lambda: Engine(device_weights(ow, world), LoopbackGroup(world),
+                                                 ShiftPolicy.fixed_tp(), cuda_graphs=False))
+    for r in range(world):
+        got, wc, fp = res[r]
+        assert len(got) == len(want)
+        for g, w in zip(got, want):
+            assert np.array_equal(np.asarray(g, dtype=np.float32), w), r
+        # every rank tracks the global cache cursors (SPMD)
+        assert wc == want_wc
+        assert fp == repr(want_fp)
