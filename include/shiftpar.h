@@ -38,6 +38,10 @@ typedef int sp_status;
 #define SP_EPI_SWIGLU 3     /* D(bf16)  = silu(acc[:, gate]) * acc[:, up]; B rows interleaved
                                in 128-row chunks [gate 128 | up 128], D width N/2 */
 #define SP_EPI_GELU 4       /* D(bf16)  = gelu_tanh(acc) (reference-compat MLP) */
+#define SP_EPI_PARTIAL_F32 5 /* D(f32) = n raw K-split partial sums [n][M][N] (ldd = N),
+                                n = sp_gemm_partials(M, N, K); the consumer sums them in
+                                ascending order (sp_add_rmsnorm n_add) — the split-K
+                                reduction fused into the next kernel */
 
 /* -------------------------------------------------------------- runtime */
 const char* sp_last_error(void);
@@ -64,19 +68,24 @@ sp_status sp_device_check(int* sm_count);
  *    D + (n / peer_width) * peer_stride + m * ldd + (n % peer_width)
  *    (the per-peer contiguous send layout of the SP seq->head all-to-all,
  *    i.e. the pack fused into the epilogue).
- * Fixed tiling, no split-K: each D element is one ascending-K reduction
+ * Fixed tiling: for M > 128 each D element is one ascending-K reduction
  * independent of M and of the N window -> row/column splits are bit-exact
- * (the property of tensor_core.py:1-28 the SP path relies on).
+ * (the property of tensor_core.py:1-28 the SP path relies on).  For M <= 128
+ * (decode) the weight is streamed swap-AB over 256-row super tiles with K
+ * split just enough to cover the SMs; split partials are summed in ascending
+ * split order (deterministic within the regime).
  */
 sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_chunk_stride,
                        const void* B, int64_t ldb, void* D, int64_t ldd, int M, int N, int K,
                        int epilogue, int64_t peer_width, int64_t peer_stride, void* stream);
-/* Device workspace for the small-M (decode) regime: when one 128-row M tile
- * cannot cover the SMs, the GEMM splits K over BN=64 tiles, writes f32
- * partials here and reduces them in ascending split order (deterministic)
- * before the epilogue.  NULL disables split-K.  Results are identical within
- * a regime; across regimes they differ at f32 rounding level. */
+/* Device workspace for the small-M (decode) regime: split-K partials are
+ * written here and reduced in ascending split order (deterministic) before
+ * the epilogue.  NULL disables split-K.  Results are identical within a
+ * regime; across regimes they differ at f32 rounding level. */
 sp_status sp_gemm_set_workspace(void* ws, int64_t bytes);
+/* Number of f32 [M][N] partial slabs SP_EPI_PARTIAL_F32 writes for this shape
+ * (1 outside the split-K regime).  Host-only, deterministic. */
+int sp_gemm_partials(int M, int N, int K);
 
 /* ------------------------------------------------ embedding / norms
  * Embedding gather (parallel_engine.py:339-346 TP, :462-469 SP): out[r, :] =
@@ -88,12 +97,14 @@ sp_status sp_embed(const int32_t* ids, const void* table_bf16, const int32_t* po
 
 /* Fused residual-add + RMSNorm (tensor_core.py:115-123 at parallel_engine.py
  * :354,:372,:390,:477,:516,:533):
- *   if add != NULL: x[r] += add[r]   (written back — the TP all-reduce result)
+ *   if add != NULL: x[r] += sum_{s < n_add} add[s][r]   (ascending s; written
+ *                   back — the TP all-reduce result, or the K-split partials
+ *                   of a SP_EPI_PARTIAL_F32 projection: [n_add][rows][hidden])
  *   out[r] = bf16( gain * x[r] / sqrt(mean(x[r]^2) + eps) )
  * If row_idx != NULL, input row r is x[row_idx[r]] (final norm on end rows).
  */
-sp_status sp_add_rmsnorm(float* x, int64_t ldx, const float* add, const float* gain, float eps,
-                         const int32_t* row_idx, void* out_bf16, int64_t ldo, int rows,
+sp_status sp_add_rmsnorm(float* x, int64_t ldx, const float* add, int n_add, const float* gain,
+                         float eps, const int32_t* row_idx, void* out_bf16, int64_t ldo, int rows,
                          int hidden, void* stream);
 
 /* ----------------------------------------------- RoPE + paged KV write

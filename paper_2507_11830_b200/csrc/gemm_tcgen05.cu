@@ -1105,6 +1105,34 @@ static int launch(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_chunk_
   return kOk;
 }
 
+// K splits of the swap-AB regime: split only until ~2/3 of the SMs stream
+// weights (all SMs when two CTAs share one), in ONE round of items — a CTA
+// with ~200 KB in flight streams well above its 1/148 share of HBM, so
+// partial SM coverage still saturates HBM, while a second round would leave a
+// tail.  Tuning override: SP_SWAP_MIN_CTAS.
+template <int NT>
+static int64_t swap_splits(int N, int K, int sms) {
+  using namespace sp::gemm;
+  using T = SwapTile<NT>;
+  const int64_t k_blocks = cdiv(K, BK);
+  const int64_t n_super = cdiv(N, swp::WT * 128);
+  const int64_t slots = (int64_t)sms * T::CTAS_PER_SM;
+  int64_t min_ctas = T::CTAS_PER_SM == 2 ? sms : (2 * sms) / 3;  // measured best (tools/swap_probe.py)
+  if (const char* e = getenv("SP_SWAP_MIN_CTAS")) min_ctas = atoi(e);
+  int64_t ks = 1;
+  while (n_super * ks < min_ctas && ks * 2 <= k_blocks) ++ks;
+  while (ks > 1 && n_super * ks > slots) --ks;
+  const int64_t per = cdiv(k_blocks, ks);
+  return cdiv(k_blocks, per);
+}
+
+// the swap-AB (decode) regime applies: one 128-row M tile that cannot cover the SMs
+static bool swap_regime(int M, int N, int sms) {
+  using namespace sp::gemm;
+  return cdiv(M, BM) == 1 && cdiv(N, 256) < sms && N % 32 == 0 &&
+         getenv("SP_GEMM_NO_SPLITK") == nullptr;
+}
+
 template <int NT>
 static int launch_swap(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_chunk_stride,
                        const void* B, int64_t ldb, void* D, int64_t ldd, int M, int N, int K,
@@ -1116,17 +1144,17 @@ static int launch_swap(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   const int64_t k_blocks = cdiv(K, BK);
   const int64_t n_super = cdiv(N, swp::WT * 128);
   const int64_t slots = (int64_t)sms * T::CTAS_PER_SM;
-  // Split K only until ~2/3 of the SMs stream weights (one round of items: a
-  // CTA with ~200 KB in flight streams well above its 1/148 share of HBM, so
-  // partial SM coverage still saturates HBM, while a second round would leave
-  // a tail).  Tuning override: SP_SWAP_MIN_CTAS.
-  int64_t min_ctas = T::CTAS_PER_SM == 2 ? sms : (2 * sms) / 3;  // measured best (tools/swap_probe.py)
-  if (const char* e = getenv("SP_SWAP_MIN_CTAS")) min_ctas = atoi(e);
-  int64_t ks = 1;
-  while (n_super * ks < min_ctas && ks * 2 <= k_blocks) ++ks;
-  while (ks > 1 && n_super * ks > slots) --ks;
+  const int64_t ks = swap_splits<NT>(N, K, sms);
   const int64_t per = cdiv(k_blocks, ks);
-  ks = cdiv(k_blocks, per);
+  const bool partial = epilogue == SP_EPI_PARTIAL_F32;
+  if (partial) {  // raw split partials go to the caller's D ([ks][M][N]); no reduce here
+    if (ks > 1) {
+      ws = static_cast<float*>(D);
+      ws_bytes = ks * (int64_t)M * N * 4;
+    } else {
+      epilogue = SP_EPI_STORE_F32;
+    }
+  }
   if (ks > 1 && (!ws || ks * (int64_t)M * N * 4 > ws_bytes)) return -1;  // caller falls back
   CUtensorMap tx, tw;
   {
@@ -1175,7 +1203,7 @@ static int launch_swap(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   const int grid = (int)std::min<int64_t>(p.num_tiles, slots);
   launch_k(gemm_swap_kernel<NT>, grid, NUM_THREADS, T::SMEM_BYTES, reinterpret_cast<cudaStream_t>(stream), tx, tw, p);
   if (int rc = check_launch("gemm_swap_kernel")) return rc;
-  if (ks > 1) {
+  if (ks > 1 && !partial) {
     const int n_out = epilogue == SP_EPI_SWIGLU ? N / 2 : N;
     const int64_t threads = (int64_t)M * (n_out / 8);
     launch_k(splitk_reduce_kernel, (unsigned)cdiv(threads, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream), p);
@@ -1251,6 +1279,16 @@ extern "C" sp_status sp_gemm_set_workspace(void* ws, int64_t bytes) {
   return kOk;
 }
 
+extern "C" int sp_gemm_partials(int M, int N, int K) {
+  using namespace sp::gemm;
+  if (M <= 0 || N <= 0 || K <= 0) return 1;
+  const int sms = sm_count();
+  if (!swap_regime(M, N, sms)) return 1;
+  if (M <= 32) return (int)swap_splits<32>(N, K, sms);
+  if (M <= 64) return (int)swap_splits<64>(N, K, sms);
+  return (int)swap_splits<128>(N, K, sms);
+}
+
 extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
                                   int64_t a_chunk_stride, const void* B, int64_t ldb, void* D,
                                   int64_t ldd, int M, int N, int K, int epilogue,
@@ -1259,8 +1297,10 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
   if (M < 0 || N <= 0 || K <= 0) return fail(kInvalid, "gemm: bad M/N/K");
   if (M == 0) return kOk;
   if (!A || !B || !D) return fail(kInvalid, "gemm: null pointer");
-  if (epilogue < SP_EPI_STORE_BF16 || epilogue > SP_EPI_GELU)
+  if (epilogue < SP_EPI_STORE_BF16 || epilogue > SP_EPI_PARTIAL_F32)
     return fail(kInvalid, "gemm: unknown epilogue");
+  if (epilogue == SP_EPI_PARTIAL_F32 && (peer_width > 0 || ldd != N))
+    return fail(kInvalid, "gemm: partial epilogue needs a dense [n][M][N] D (ldd == N)");
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
     return fail(kInvalid, "gemm: A/B must be 16-byte aligned");
   if (lda % 8 || ldb % 8 || ldd % 8) return fail(kInvalid, "gemm: leading dims must be multiples of 8");
@@ -1282,10 +1322,9 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
   const int sms = sm_count();
   const int64_t m_tiles = cdiv(M, BM);
   const int64_t k_blocks = cdiv(K, BK);
-  const bool no_split = getenv("SP_GEMM_NO_SPLITK") != nullptr;
   int bn = 256;
   if (m_tiles * cdiv(N, 256) < sms) {
-    if (m_tiles == 1 && !no_split && N % 32 == 0) {
+    if (swap_regime(M, N, sms)) {
       // decode-size M: swap-AB weight streaming (+ split-K / fused epilogue)
       int rc = -1;
       if (M <= 32)
@@ -1309,6 +1348,7 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
       }
     }
   }
+  if (epilogue == SP_EPI_PARTIAL_F32) epilogue = SP_EPI_STORE_F32;  // one "partial" = the result
   if (const char* f = getenv("SP_GEMM_FORCE_BN")) {
     const int fb = atoi(f);
     if ((fb == 32 || fb == 64 || fb == 128 || fb == 256) && epilogue != SP_EPI_SWIGLU) bn = fb;

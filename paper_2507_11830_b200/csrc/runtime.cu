@@ -66,7 +66,8 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const __nv_bfloat1
 // ------------------------------------------------------- add + rmsnorm
 template <int VEC>
 __global__ void add_rmsnorm_kernel(float* __restrict__ x, int64_t ldx, const float* __restrict__ add,
-                                   const float* __restrict__ gain, float eps,
+                                   int n_add, int64_t add_stride, const float* __restrict__ gain,
+                                   float eps,
                                    const int32_t* __restrict__ row_idx,
                                    __nv_bfloat16* __restrict__ out, int64_t ldo, int hidden) {
   pdl_wait();  // inputs of this kernel are written by its predecessor
@@ -84,7 +85,14 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, int64_t ldx, const flo
     if (c < hidden) {
       t = *reinterpret_cast<const float4*>(xr + c);
       if (ar) {
-        float4 a = *reinterpret_cast<const float4*>(ar + c);
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int s = 0; s < n_add; ++s) {  // ascending: the split-K / all-reduce order
+          const float4 b = *reinterpret_cast<const float4*>(ar + s * add_stride + c);
+          a.x += b.x;
+          a.y += b.y;
+          a.z += b.z;
+          a.w += b.w;
+        }
         t.x += a.x;
         t.y += a.y;
         t.z += a.z;
@@ -334,9 +342,12 @@ extern "C" sp_status sp_embed(const int32_t* ids, const void* table_bf16, const 
   return check_launch("embed_kernel");
 }
 
-extern "C" sp_status sp_add_rmsnorm(float* x, int64_t ldx, const float* add, const float* gain,
-                                    float eps, const int32_t* row_idx, void* out_bf16, int64_t ldo,
-                                    int rows, int hidden, void* stream) {
+extern "C" sp_status sp_add_rmsnorm(float* x, int64_t ldx, const float* add, int n_add,
+                                    const float* gain, float eps, const int32_t* row_idx,
+                                    void* out_bf16, int64_t ldo, int rows, int hidden,
+                                    void* stream) {
+  if (add && n_add < 1) return fail(kInvalid, "add_rmsnorm: n_add must be >= 1");
+  const int64_t add_stride = (int64_t)rows * hidden;
   if (rows < 0 || hidden <= 0 || hidden % 4 || ldx % 4 || ldo % 4)
     return fail(kInvalid, "add_rmsnorm: hidden and strides must be multiples of 4");
   if (rows == 0) return kOk;
@@ -345,12 +356,12 @@ extern "C" sp_status sp_add_rmsnorm(float* x, int64_t ldx, const float* add, con
   const int per = (hidden + threads * 4 - 1) / (threads * 4);
   auto out = static_cast<__nv_bfloat16*>(out_bf16);
   switch (per) {
-    case 1: launch_k(add_rmsnorm_kernel<1>, rows, threads, 0, S(stream), x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
-    case 2: launch_k(add_rmsnorm_kernel<2>, rows, threads, 0, S(stream), x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
-    case 3: launch_k(add_rmsnorm_kernel<3>, rows, threads, 0, S(stream), x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
-    case 4: launch_k(add_rmsnorm_kernel<4>, rows, threads, 0, S(stream), x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
+    case 1: launch_k(add_rmsnorm_kernel<1>, rows, threads, 0, S(stream), x, ldx, add, n_add, add_stride, gain, eps, row_idx, out, ldo, hidden); break;
+    case 2: launch_k(add_rmsnorm_kernel<2>, rows, threads, 0, S(stream), x, ldx, add, n_add, add_stride, gain, eps, row_idx, out, ldo, hidden); break;
+    case 3: launch_k(add_rmsnorm_kernel<3>, rows, threads, 0, S(stream), x, ldx, add, n_add, add_stride, gain, eps, row_idx, out, ldo, hidden); break;
+    case 4: launch_k(add_rmsnorm_kernel<4>, rows, threads, 0, S(stream), x, ldx, add, n_add, add_stride, gain, eps, row_idx, out, ldo, hidden); break;
     case 5: case 6: case 7: case 8:
-      launch_k(add_rmsnorm_kernel<8>, rows, threads, 0, S(stream), x, ldx, add, gain, eps, row_idx, out, ldo, hidden); break;
+      launch_k(add_rmsnorm_kernel<8>, rows, threads, 0, S(stream), x, ldx, add, n_add, add_stride, gain, eps, row_idx, out, ldo, hidden); break;
     default: return fail(kUnsupported, "add_rmsnorm: hidden > 8192");
   }
   return check_launch("add_rmsnorm_kernel");

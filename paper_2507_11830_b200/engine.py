@@ -587,10 +587,15 @@ class Engine:
         # fused one-shot all-reduce over peer memory (partials -> peers' sum in the norm kernel)
         peer = self._peer if (self._peer is not None and M <= self._peer.max_tokens) else None
         peer_pending = False
+        split_pending = None  # (K-split partials of the last projection, count) -> next norm
         for layer in range(n_full):
             lw = w.layers[layer]
             if peer_pending:
                 ops.peer_allreduce_add_rmsnorm(peer.part_ptrs[1], P, x, lw.attn_gain, eps, xn, M)
+            elif split_pending is not None:
+                ops.add_rmsnorm(x, lw.attn_gain, eps, xn, add=split_pending[0],
+                                n_add=split_pending[1])
+                split_pending = None
             else:
                 ops.add_rmsnorm(x, lw.attn_gain, eps, xn, add=pending)
             self._stage_all(layer, batch)
@@ -605,8 +610,8 @@ class Engine:
                 self._attend(r, layer, q, o, meta, meters[r])
                 wo = lw.wo[:, r * hqw:]
                 if P == 1:
-                    ops.gemm(o, wo, x, ops.EPI_ADD_F32, M=M, N=h, K=hqw, lda=hqw,
-                             ldb=cfg.n_heads * d, ldd=h, meter=meters[r])
+                    split_pending = self._proj_residual(o, wo, x, M, h, hqw, cfg.n_heads * d,
+                                                        meters[r], fuse=True)
                 else:
                     part = (peer.part[r][0][:M] if peer is not None
                             else torch.empty((M, h), dtype=torch.float32, device=dev))
@@ -619,6 +624,10 @@ class Engine:
             if peer is not None:
                 self._peer_reduce_wait(0, parts)
                 ops.peer_allreduce_add_rmsnorm(peer.part_ptrs[0], P, x, lw.mlp_gain, eps, xn2, M)
+            elif split_pending is not None:
+                ops.add_rmsnorm(x, lw.mlp_gain, eps, xn2, add=split_pending[0],
+                                n_add=split_pending[1])
+                split_pending = None
             else:
                 red = g.all_reduce_sum(parts)[g.local_ranks[0]] if P > 1 else None
                 ops.add_rmsnorm(x, lw.mlp_gain, eps, xn2, add=red)
@@ -628,8 +637,9 @@ class Engine:
                 self._mlp_up(xn2, lw, r, act, M, meters[r])
                 wd = lw.wdown[:, r * fl:]
                 if P == 1:
-                    ops.gemm(act, wd, x, ops.EPI_ADD_F32, M=M, N=h, K=fl, lda=fl,
-                             ldb=cfg.ffn_dim, ldd=h, meter=meters[r])
+                    # the last layer's sum must land in x before the final norm
+                    split_pending = self._proj_residual(act, wd, x, M, h, fl, cfg.ffn_dim,
+                                                        meters[r], fuse=layer < n_full - 1)
                 else:
                     part = (peer.part[r][1][:M] if peer is not None
                             else torch.empty((M, h), dtype=torch.float32, device=dev))
@@ -675,6 +685,19 @@ class Engine:
         g.charge("all_reduce", [2.0 * (P - 1) / P * t.numel() * t.element_size()] * P)
         for r in g.local_ranks:
             ops.peer_wait(peer.flags[r][2 + which], P)
+
+    def _proj_residual(self, a, w, x, M, N, K, ldb, meter, fuse: bool):
+        """x += a · w^T (residual projection, P = 1).  In the split-K (decode)
+        regime with `fuse`, leave the K-split partials for the next add+RMSNorm
+        to sum (no reduce kernel) and return (partials, count); else add in place."""
+        n = ops.gemm_partials(M, N, K) if fuse else 1
+        if n > 1:
+            parts = torch.empty((n, M, N), dtype=torch.float32, device=x.device)
+            ops.gemm(a, w, parts, ops.EPI_PARTIAL_F32, M=M, N=N, K=K, lda=K, ldb=ldb, ldd=N,
+                     meter=meter)
+            return parts, n
+        ops.gemm(a, w, x, ops.EPI_ADD_F32, M=M, N=N, K=K, lda=K, ldb=ldb, ldd=N, meter=meter)
+        return None
 
     def _mlp_up(self, xn2, lw, r, act, rows, meter):
         cfg = self.config
@@ -789,12 +812,18 @@ class Engine:
         in_fwd = {r: [rows[r]] * P for r in range(P)}
         out_fwd = {s: list(rows) for s in range(P)}
         peer = self._peer if (self._peer is not None and M <= self._peer.max_tokens) else None
+        split_pending = None  # P = 1: K-split partials of the last projection -> next norm
         for layer in range(n_full):
             lw = w.layers[layer]
             send, recv = {}, {}
             for r in g.local_ranks:
                 xn = torch.empty((rows[r], h), dtype=torch.bfloat16, device=dev)
-                ops.add_rmsnorm(xs[r], lw.attn_gain, eps, xn)
+                if split_pending is not None:
+                    ops.add_rmsnorm(xs[r], lw.attn_gain, eps, xn, add=split_pending[0],
+                                    n_add=split_pending[1])
+                    split_pending = None
+                else:
+                    ops.add_rmsnorm(xs[r], lw.attn_gain, eps, xn)
                 if peer is not None:
                     # fused seq->head all-to-all: the epilogue stores rank s's q|k|v
                     # heads straight into s's receive buffer at this shard's rows
@@ -846,13 +875,28 @@ class Engine:
                 g.all_to_all(att, back, {r: list(rows) for r in range(P)},
                              {s: [rows[s]] * P for s in range(P)}, row_bytes=hqw * 2)
             for r in g.local_ranks:
-                self._o_proj_sp(back[r], lw, xs[r], rows[r], meters[r])
                 xn2 = torch.empty((rows[r], h), dtype=torch.bfloat16, device=dev)
-                ops.add_rmsnorm(xs[r], lw.mlp_gain, eps, xn2)
+                if P == 1:  # split-K partials summed by the norm (no reduce kernel)
+                    sp_o = self._proj_residual(back[r], lw.wo, xs[r], rows[r], h,
+                                               cfg.n_heads * d, cfg.n_heads * d, meters[r],
+                                               fuse=True)
+                    if sp_o is not None:
+                        ops.add_rmsnorm(xs[r], lw.mlp_gain, eps, xn2, add=sp_o[0], n_add=sp_o[1])
+                    else:
+                        ops.add_rmsnorm(xs[r], lw.mlp_gain, eps, xn2)
+                else:
+                    self._o_proj_sp(back[r], lw, xs[r], rows[r], meters[r])
+                    ops.add_rmsnorm(xs[r], lw.mlp_gain, eps, xn2)
                 act = torch.empty((rows[r], cfg.ffn_dim), dtype=torch.bfloat16, device=dev)
                 self._mlp_up_full(xn2, lw, act, rows[r], meters[r])
-                ops.gemm(act, lw.wdown, xs[r], ops.EPI_ADD_F32, M=rows[r], N=h, K=cfg.ffn_dim,
-                         lda=cfg.ffn_dim, ldb=cfg.ffn_dim, ldd=h, meter=meters[r])
+                if P == 1:
+                    split_pending = self._proj_residual(
+                        act, lw.wdown, xs[r], rows[r], h, cfg.ffn_dim, cfg.ffn_dim, meters[r],
+                        fuse=layer < n_full - 1 and cut is None)
+                else:
+                    ops.gemm(act, lw.wdown, xs[r], ops.EPI_ADD_F32, M=rows[r], N=h,
+                             K=cfg.ffn_dim, lda=cfg.ffn_dim, ldb=cfg.ffn_dim, ldd=h,
+                             meter=meters[r])
         if cut is not None:
             return self._tail_sp(meta, batch, meters, xs, cut)
         parts = {}

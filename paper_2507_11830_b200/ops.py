@@ -21,6 +21,7 @@ EPI_STORE_F32 = 1
 EPI_ADD_F32 = 2
 EPI_SWIGLU = 3
 EPI_GELU = 4
+EPI_PARTIAL_F32 = 5  # raw K-split partials [n][M][N], n = gemm_partials(M, N, K)
 
 launch_count = 0
 
@@ -101,6 +102,8 @@ def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, epilogue: int, *, M:
         _need(d, torch.bfloat16, "gemm D")
     else:
         _need(d, torch.float32, "gemm D")
+    if epilogue == EPI_PARTIAL_F32 and d.numel() < gemm_partials(M, N, K) * M * N:
+        raise ContractViolation("gemm: partial epilogue needs [gemm_partials(M,N,K), M, N] f32 D")
     if meter is not None:
         meter.add_matmul(M, K, N)
     if M == 0:
@@ -195,9 +198,15 @@ def embed(ids: torch.Tensor, table: torch.Tensor, out: torch.Tensor,
     _count()
 
 
+def gemm_partials(M: int, N: int, K: int) -> int:
+    """How many f32 [M, N] partial slabs an EPI_PARTIAL_F32 GEMM writes."""
+    return int(_lib.load().sp_gemm_partials(M, N, K))
+
+
 def add_rmsnorm(x: torch.Tensor, gain: torch.Tensor, eps: float, out: torch.Tensor, *,
                 add: Optional[torch.Tensor] = None, row_idx: Optional[torch.Tensor] = None,
-                rows: Optional[int] = None) -> None:
+                rows: Optional[int] = None, n_add: int = 1) -> None:
+    """out = bf16(rms_norm(x (+)= sum of n_add [rows, h] slabs of `add`))."""
     _need(x, torch.float32, "rmsnorm x")
     _need(gain, torch.float32, "rmsnorm gain")
     _need(out, torch.bfloat16, "rmsnorm out")
@@ -205,7 +214,11 @@ def add_rmsnorm(x: torch.Tensor, gain: torch.Tensor, eps: float, out: torch.Tens
     if n == 0:
         return
     h = x.shape[1]
-    rc = _lib.load().sp_add_rmsnorm(x.data_ptr(), x.stride(0), _ptr(add), gain.data_ptr(),
+    if add is not None:
+        _need(add, torch.float32, "rmsnorm add")
+        if add.numel() < n_add * n * h:
+            raise ContractViolation("add_rmsnorm: add holds fewer than n_add [rows, h] slabs")
+    rc = _lib.load().sp_add_rmsnorm(x.data_ptr(), x.stride(0), _ptr(add), n_add, gain.data_ptr(),
                                     float(eps), _ptr(row_idx), out.data_ptr(), out.stride(0), n, h,
                                     _stream())
     _lib.check(rc, "sp_add_rmsnorm")
