@@ -30,6 +30,42 @@ namespace attn_tc {
 constexpr int HD = 128;
 constexpr int QROWS = 128;       // rows per Q tile
 constexpr int KT = 128;          // keys per tile
+// Two measured-negative softmax variants kept as build knobs (tools/kbench.py attn,
+// 8K causal): one MUFU.EX2.bf16x2 per pair (1023 vs 1051 TFLOP/s) and an
+// FMA-pipe polynomial for part of the pairs (1-4% slower).  ncu shows the SFU
+// at ~54% and the softmax warps mostly waiting for S: the ping-pong schedule,
+// not the exponential, bounds this kernel.
+#ifndef ATTN_EXP_BF16X2
+#define ATTN_EXP_BF16X2 0
+#endif
+#ifndef ATTN_POLY_PAIRS
+#define ATTN_POLY_PAIRS 0
+#endif
+constexpr int kPolyPairs = ATTN_POLY_PAIRS;  // of 32 pairs per 64 columns (tools/kbench.py attn)
+
+// 2^x, x <= 0, for a PAIR of lanes on the FMA/ALU pipes: round-to-nearest
+// split x = n + r (magic-number add, |r| <= 1/2), cubic 2^r (rel err 1.8e-4,
+// far below the bf16 rounding of P), exponent n added into the bits.  x is
+// clamped at -126 (2^-126 ~ 0 next to the row max's 1).
+__device__ __forceinline__ void exp2_poly2(uint64_t x2, float& a, float& b) {
+  float xa, xb;
+  f2_unpack(x2, xa, xb);
+  x2 = f2_pack(fmaxf(xa, -126.f), fmaxf(xb, -126.f));
+  const uint64_t magic = f2_pack(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const uint64_t y = f2_add(x2, magic);                   // n in the low mantissa bits
+  const uint64_t n = f2_add(y, f2_pack(-12582912.f, -12582912.f));
+  const uint64_t r = f2_fma(n, f2_pack(-1.f, -1.f), x2);  // x - n
+  uint64_t p = f2_fma(f2_pack(0.0546027f, 0.0546027f), r, f2_pack(0.24192398f, 0.24192398f));
+  p = f2_fma(p, r, f2_pack(0.69331645f, 0.69331645f));
+  p = f2_fma(p, r, f2_pack(1.f, 1.f));
+  float pa, pb, ya, yb;
+  f2_unpack(p, pa, pb);
+  f2_unpack(y, ya, yb);
+  // bits(y) << 23 == n << 23 (mod 2^32): the magic's own bits shift out
+  a = __int_as_float(__float_as_int(pa) + (__float_as_int(ya) << 23));
+  b = __int_as_float(__float_as_int(pb) + (__float_as_int(yb) << 23));
+}
+
 constexpr int NUM_THREADS = 384;  // 3 warpgroups: softmax 0, softmax 1, producer/MMA
 constexpr int Q_TILE_BYTES = QROWS * HD * 2;      // 32 KiB (two 64-wide d chunks)
 constexpr int KV_TILE_BYTES = KT * HD * 2;        // 32 KiB
@@ -288,7 +324,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         tmem_st_wait();
       }
-      // p = 2^(raw * scale - m_run): FFMA2 + 2 x MUFU.EX2 + FADD2 per pair
+      // p = 2^(raw * scale - m_run): FFMA2 + 2 x MUFU.EX2 (or the FMA-pipe
+      // polynomial for the last kPolyPairs pairs of each 64 columns, so the
+      // SFU is not the co-bottleneck with the tensor core) + FADD2 per pair
       const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2);
       const uint64_t nm2 = f2_pack(-m_run, -m_run);
       uint64_t sum2 = f2_pack(0.f, 0.f);
@@ -298,9 +336,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
           float a, b;
-          f2_unpack(f2_fma(f2_pack(s[c * 64 + 2 * e], s[c * 64 + 2 * e + 1]), sc2, nm2), a, b);
-          a = fast_exp2(a);
-          b = fast_exp2(b);
+          const uint64_t x2 = f2_fma(f2_pack(s[c * 64 + 2 * e], s[c * 64 + 2 * e + 1]), sc2, nm2);
+#if ATTN_EXP_BF16X2
+          if (true) {  // one MUFU.EX2 per PAIR: exponent rounded to bf16, P produced as bf16x2
+            f2_unpack(x2, a, b);
+            uint32_t pb;
+            asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(pb) : "r"(pack_bf16x2(a, b)));
+            const float2 pf = unpack_bf16x2(pb);
+            sum2 = f2_add(sum2, f2_pack(pf.x, pf.y));
+            pk[e] = pb;
+            continue;
+          }
+#endif
+          if (e >= 32 - kPolyPairs) {
+            exp2_poly2(x2, a, b);
+          } else {
+            f2_unpack(x2, a, b);
+            a = fast_exp2(a);
+            b = fast_exp2(b);
+          }
           sum2 = f2_add(sum2, f2_pack(a, b));
           pk[e] = pack_bf16x2(a, b);
         }

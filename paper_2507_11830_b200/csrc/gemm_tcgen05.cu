@@ -414,7 +414,10 @@ struct SwapTile {
   // M <= 32 (latency-bound decode): two CTAs per SM, so a successor's CTAs can
   // start streaming weights (PDL) while this one drains; larger M: one CTA per
   // SM with a ~200 KB ring.
-  static constexpr int CTAS_PER_SM = NT <= 32 ? 2 : 1;
+#ifndef SWAP_CPS_MAX_NT
+#define SWAP_CPS_MAX_NT 32
+#endif
+  static constexpr int CTAS_PER_SM = NT <= SWAP_CPS_MAX_NT ? 2 : 1;
   static constexpr int RING = (CTAS_PER_SM == 2 ? 108 : 200) * 1024;
   static constexpr int STAGES = RING / STAGE_BYTES > 10 ? 10 : RING / STAGE_BYTES;
   static constexpr int ACC_COLS = swp::WT * NT;  // one accumulator stage
