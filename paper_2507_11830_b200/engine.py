@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import enum
 import time
+import warnings
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence as Seq, Tuple
 
@@ -202,6 +203,7 @@ class _GraphEntry:
         self.outputs: List[torch.Tensor] = []
         self.charges: list = []
         self.kernels = 0
+        self.failed = False  # capture raised: this key stays eager
 
 
 class Engine:
@@ -327,7 +329,7 @@ class Engine:
         else:
             fwd = self._forward_tp if mode is ParallelMode.TP else self._forward_sp
             logits = fwd(meta, batch, meters, span_logits, cut)
-            if graph_key is not None:
+            if graph_key is not None and not self._graphs[graph_key].failed:
                 self._capture(graph_key, meta, batch, fwd)
         for it in batch.items:
             it.seq.cache.commit(len(it.tokens))
@@ -363,6 +365,12 @@ class Engine:
         try:
             with torch.cuda.graph(graph, pool=self._graph_pool):
                 outs = fwd(meta, batch, [FlopMeter() for _ in range(self.world_size)], False, None)
+        except RuntimeError as e:
+            # e.g. a collective backend that cannot be captured: run this key eagerly
+            del self.group.records[n_rec:]
+            entry.failed = True
+            warnings.warn(f"CUDA-graph capture of decode pass {key} failed ({e}); running eagerly")
+            return
         finally:
             self._capturing = False
         entry.kernels = ops.kernel_launches() - k0
