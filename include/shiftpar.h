@@ -120,6 +120,14 @@ sp_status sp_rope_kv_write(const void* qkv, int64_t ldqkv, const int32_t* pos,
                            const int32_t* slot, const float* rope_table, void* q_out,
                            int64_t ldq, void* k_pool, void* v_pool, int rows, int q_heads,
                            int kv_heads, int head_dim, int block_size, void* stream);
+/* Same, reading the QKV projection as n_parts f32 K-split partials
+ * [n_parts][rows][ldqkv] (SP_EPI_PARTIAL_F32) summed in ascending order and
+ * rounded to bf16 first — the split-K reduction fused into this kernel. */
+sp_status sp_rope_kv_write_partials(const float* parts, int n_parts, int64_t ldqkv,
+                                    const int32_t* pos, const int32_t* slot,
+                                    const float* rope_table, void* q_out, int64_t ldq,
+                                    void* k_pool, void* v_pool, int rows, int q_heads,
+                                    int kv_heads, int head_dim, int block_size, void* stream);
 
 /* ----------------------------------------------------- paged attention
  * Replaces attend_cached (tensor_core.py:135-176) looped per (item, head)

@@ -137,7 +137,33 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, int64_t ldx, const flo
 // 8 threads per (token, head): thread j owns rotation pairs [8j, 8j+8) of a
 // 128-dim head (16-byte loads of both halves, one float4x2 of cos/sin each);
 // generic head_dim falls back to one pair per lane.
-__global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldqkv,
+// 8 consecutive values at column c of row r: the bf16 qkv row, or (parts !=
+// NULL) the ascending sum of n_parts f32 K-split partials [n][rows][ldqkv]
+// rounded to bf16 — the split-K reduction of the QKV projection fused here,
+// bit-identical to reducing first (same order, same final rounding).
+__device__ __forceinline__ uint4 qkv_chunk(const __nv_bfloat16* qkv, const float* parts, int n_parts,
+                                           int64_t ldqkv, int rows, int r, int64_t c) {
+  if (parts == nullptr) return *reinterpret_cast<const uint4*>(qkv + (int64_t)r * ldqkv + c);
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = 0.f;
+  for (int s = 0; s < n_parts; ++s) {
+    const float* src = parts + ((int64_t)s * rows + r) * ldqkv + c;
+    const float4 a = *reinterpret_cast<const float4*>(src);
+    const float4 b = *reinterpret_cast<const float4*>(src + 4);
+    v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
+    v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+  }
+  uint4 u;
+  u.x = pack_bf16x2(v[0], v[1]);
+  u.y = pack_bf16x2(v[2], v[3]);
+  u.z = pack_bf16x2(v[4], v[5]);
+  u.w = pack_bf16x2(v[6], v[7]);
+  return u;
+}
+
+__global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, const float* __restrict__ parts,
+                               int n_parts, int64_t ldqkv,
                                const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,
                                const float* __restrict__ rope, __nv_bfloat16* __restrict__ q_out,
                                int64_t ldq, __nv_bfloat16* __restrict__ k_pool,
@@ -154,7 +180,7 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld
   const int j = (int)(gid % tpg);
   const int r = (int)(item / heads);
   const int h = (int)(item % heads);
-  const __nv_bfloat16* src = qkv + (int64_t)r * ldqkv + (int64_t)h * head_dim;
+  const int64_t col = (int64_t)h * head_dim;
   __nv_bfloat16* dst;
   if (h < q_heads) {
     if (!q_out) return;
@@ -169,8 +195,8 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld
   }
   const bool rotate = rope != nullptr && h < q_heads + kv_heads;
   const int i0 = j * 8;
-  uint4 ua = *reinterpret_cast<const uint4*>(src + i0);
-  uint4 ub = *reinterpret_cast<const uint4*>(src + half + i0);
+  uint4 ua = qkv_chunk(qkv, parts, n_parts, ldqkv, rows, r, col + i0);
+  uint4 ub = qkv_chunk(qkv, parts, n_parts, ldqkv, rows, r, col + half + i0);
   if (rotate) {
     const float4* cs = reinterpret_cast<const float4*>(rope + ((int64_t)pos[r] * half + i0) * 2);
     uint32_t* pa = reinterpret_cast<uint32_t*>(&ua);
@@ -367,11 +393,37 @@ extern "C" sp_status sp_add_rmsnorm(float* x, int64_t ldx, const float* add, int
   return check_launch("add_rmsnorm_kernel");
 }
 
+static sp_status rope_kv_launch(const void* qkv, const float* parts, int n_parts, int64_t ldqkv,
+                                const int32_t* pos, const int32_t* slot, const float* rope_table,
+                                void* q_out, int64_t ldq, void* k_pool, void* v_pool, int rows,
+                                int q_heads, int kv_heads, int head_dim, int block_size,
+                                void* stream);
+
 extern "C" sp_status sp_rope_kv_write(const void* qkv, int64_t ldqkv, const int32_t* pos,
                                       const int32_t* slot, const float* rope_table, void* q_out,
                                       int64_t ldq, void* k_pool, void* v_pool, int rows,
                                       int q_heads, int kv_heads, int head_dim, int block_size,
                                       void* stream) {
+  return rope_kv_launch(qkv, nullptr, 0, ldqkv, pos, slot, rope_table, q_out, ldq, k_pool, v_pool,
+                        rows, q_heads, kv_heads, head_dim, block_size, stream);
+}
+
+extern "C" sp_status sp_rope_kv_write_partials(const float* parts, int n_parts, int64_t ldqkv,
+                                               const int32_t* pos, const int32_t* slot,
+                                               const float* rope_table, void* q_out, int64_t ldq,
+                                               void* k_pool, void* v_pool, int rows, int q_heads,
+                                               int kv_heads, int head_dim, int block_size,
+                                               void* stream) {
+  if (!parts || n_parts < 1) return fail(kInvalid, "rope_kv_write_partials: need >= 1 partial");
+  return rope_kv_launch(nullptr, parts, n_parts, ldqkv, pos, slot, rope_table, q_out, ldq, k_pool,
+                        v_pool, rows, q_heads, kv_heads, head_dim, block_size, stream);
+}
+
+static sp_status rope_kv_launch(const void* qkv, const float* parts, int n_parts, int64_t ldqkv,
+                                const int32_t* pos, const int32_t* slot, const float* rope_table,
+                                void* q_out, int64_t ldq, void* k_pool, void* v_pool, int rows,
+                                int q_heads, int kv_heads, int head_dim, int block_size,
+                                void* stream) {
   if (rows < 0 || q_heads < 0 || kv_heads < 0 || head_dim <= 0 || head_dim % 2 || block_size <= 0)
     return fail(kInvalid, "rope_kv_write: bad geometry");
   if (rows == 0 || q_heads + kv_heads == 0) return kOk;
@@ -381,7 +433,7 @@ extern "C" sp_status sp_rope_kv_write(const void* qkv, int64_t ldqkv, const int3
   const int heads = q_heads + 2 * kv_heads;
   const int64_t threads = (int64_t)rows * heads * (head_dim / 16);
   launch_k(rope_kv_kernel, (unsigned)((threads + 255) / 256), 256, 0, S(stream),
-           static_cast<const __nv_bfloat16*>(qkv), ldqkv, pos, slot, rope_table,
+           static_cast<const __nv_bfloat16*>(qkv), parts, n_parts, ldqkv, pos, slot, rope_table,
            static_cast<__nv_bfloat16*>(q_out), ldq, static_cast<__nv_bfloat16*>(k_pool),
            static_cast<__nv_bfloat16*>(v_pool), rows, q_heads, kv_heads, head_dim, block_size);
   return check_launch("rope_kv_kernel");

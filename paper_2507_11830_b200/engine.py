@@ -29,6 +29,7 @@ mode can change every pass with zero KV movement (kv_cache.py:1-15).
 from __future__ import annotations
 
 import enum
+import os
 import time
 import warnings
 from dataclasses import dataclass, field
@@ -252,6 +253,7 @@ class Engine:
         # attention split-KV workspace, allocated once (graph replays need static buffers)
         self._ws = torch.empty(16 << 20, dtype=torch.float32, device=self.device)
         self.cuda_graphs = cuda_graphs
+        self._fuse_splitk = os.environ.get("SP_FUSE_SPLITK", "1") != "0"
         self._graphs: Dict[tuple, _GraphEntry] = {}
         self._graph_pool = torch.cuda.graph_pool_handle() if cuda_graphs else None
         self._capturing = False
@@ -548,10 +550,19 @@ class Engine:
 
     def _kv_write(self, r: int, layer: int, qkv: torch.Tensor, q_out: Optional[torch.Tensor],
                   meta: _Meta, batch: Batch, *, q_heads: Optional[int] = None,
-                  pos=None, slots=None, rows=None) -> None:
+                  pos=None, slots=None, rows=None, parts=None) -> None:
         cfg = self.config
         P = self.world_size
         hq = cfg.n_heads // P if q_heads is None else q_heads
+        if parts is not None:
+            ops.rope_kv_write_partials(parts[0], parts[1], meta.pos if pos is None else pos,
+                                       meta.slots if slots is None else slots, self.weights.rope,
+                                       q_out, self.pool.layer_k(r, layer),
+                                       self.pool.layer_v(r, layer),
+                                       rows=meta.M if rows is None else rows, q_heads=hq,
+                                       kv_heads=cfg.kv_heads // P, head_dim=cfg.head_dim,
+                                       block_size=self.pool.block_size)
+            return
         ops.rope_kv_write(qkv, meta.pos if pos is None else pos,
                           meta.slots if slots is None else slots, self.weights.rope, q_out,
                           self.pool.layer_k(r, layer), self.pool.layer_v(r, layer),
@@ -609,11 +620,18 @@ class Engine:
             self._stage_all(layer, batch)
             parts = {}
             for r in g.local_ranks:
-                qkv = torch.empty((M, W), dtype=torch.bfloat16, device=dev)
-                ops.gemm(xn, lw.wqkv[r * W:(r + 1) * W], qkv, ops.EPI_STORE_BF16, M=M, N=W, K=h,
-                         lda=h, ldb=h, ldd=W, meter=meters[r])
                 q = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
-                self._kv_write(r, layer, qkv, q, meta, batch)
+                n_qkv = self._partials(M, W, h)
+                if n_qkv > 1:  # decode: K-split partials reduced inside RoPE + KV write
+                    qparts = torch.empty((n_qkv, M, W), dtype=torch.float32, device=dev)
+                    ops.gemm(xn, lw.wqkv[r * W:(r + 1) * W], qparts, ops.EPI_PARTIAL_F32, M=M,
+                             N=W, K=h, lda=h, ldb=h, ldd=W, meter=meters[r])
+                    self._kv_write(r, layer, None, q, meta, batch, parts=(qparts, n_qkv))
+                else:
+                    qkv = torch.empty((M, W), dtype=torch.bfloat16, device=dev)
+                    ops.gemm(xn, lw.wqkv[r * W:(r + 1) * W], qkv, ops.EPI_STORE_BF16, M=M, N=W,
+                             K=h, lda=h, ldb=h, ldd=W, meter=meters[r])
+                    self._kv_write(r, layer, qkv, q, meta, batch)
                 o = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
                 self._attend(r, layer, q, o, meta, meters[r])
                 wo = lw.wo[:, r * hqw:]
@@ -694,11 +712,16 @@ class Engine:
         for r in g.local_ranks:
             ops.peer_wait(peer.flags[r][2 + which], P)
 
+    def _partials(self, M: int, N: int, K: int) -> int:
+        """K-split partial count for fusing a decode projection's reduction into
+        its consumer (1 = not split / fusion off: SP_FUSE_SPLITK=0)."""
+        return ops.gemm_partials(M, N, K) if self._fuse_splitk else 1
+
     def _proj_residual(self, a, w, x, M, N, K, ldb, meter, fuse: bool):
         """x += a · w^T (residual projection, P = 1).  In the split-K (decode)
         regime with `fuse`, leave the K-split partials for the next add+RMSNorm
         to sum (no reduce kernel) and return (partials, count); else add in place."""
-        n = ops.gemm_partials(M, N, K) if fuse else 1
+        n = self._partials(M, N, K) if fuse else 1
         if n > 1:
             parts = torch.empty((n, M, N), dtype=torch.float32, device=x.device)
             ops.gemm(a, w, parts, ops.EPI_PARTIAL_F32, M=M, N=N, K=K, lda=K, ldb=ldb, ldd=N,
@@ -840,10 +863,17 @@ class Engine:
                                       peer_width=W, meter=meters[r])
                     ops.peer_signal(peer.fwd_flag_ptrs, P, r)
                 elif P == 1:
-                    send[r] = torch.empty((M, W), dtype=torch.bfloat16, device=dev)
-                    ops.gemm(xn, lw.wqkv, send[r], ops.EPI_STORE_BF16, M=M, N=W, K=h, lda=h,
-                             ldb=h, ldd=W, meter=meters[r])
-                    recv[r] = send[r]
+                    n_qkv = self._partials(M, W, h)
+                    if n_qkv > 1:  # decode: K-split partials reduced inside RoPE + KV write
+                        qparts = torch.empty((n_qkv, M, W), dtype=torch.float32, device=dev)
+                        ops.gemm(xn, lw.wqkv, qparts, ops.EPI_PARTIAL_F32, M=M, N=W, K=h,
+                                 lda=h, ldb=h, ldd=W, meter=meters[r])
+                        recv[r] = (qparts, n_qkv)
+                    else:
+                        send[r] = torch.empty((M, W), dtype=torch.bfloat16, device=dev)
+                        ops.gemm(xn, lw.wqkv, send[r], ops.EPI_STORE_BF16, M=M, N=W, K=h, lda=h,
+                                 ldb=h, ldd=W, meter=meters[r])
+                        recv[r] = send[r]
                 else:
                     # epilogue writes rank s's q|k|v heads into send block s (fused pack)
                     send[r] = torch.empty((P * rows[r], W), dtype=torch.bfloat16, device=dev)
@@ -862,7 +892,10 @@ class Engine:
             att = {}
             for r in g.local_ranks:
                 q = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
-                self._kv_write(r, layer, recv[r], q, meta, batch)
+                if isinstance(recv[r], tuple):
+                    self._kv_write(r, layer, None, q, meta, batch, parts=recv[r])
+                else:
+                    self._kv_write(r, layer, recv[r], q, meta, batch)
                 o = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
                 self._attend(r, layer, q, o, meta, meters[r])
                 att[r] = o

@@ -241,6 +241,26 @@ def rope_kv_write(qkv: torch.Tensor, pos: torch.Tensor, slot: torch.Tensor,
     _count()
 
 
+def rope_kv_write_partials(parts: torch.Tensor, n_parts: int, pos: torch.Tensor,
+                           slot: torch.Tensor, rope: Optional[torch.Tensor],
+                           q_out: Optional[torch.Tensor], k_pool: torch.Tensor,
+                           v_pool: torch.Tensor, *, rows: int, q_heads: int, kv_heads: int,
+                           head_dim: int, block_size: int) -> None:
+    """rope_kv_write on a QKV projection left as n_parts K-split partials [n, rows, W]."""
+    _need(parts, torch.float32, "rope partials")
+    if rows == 0:
+        return
+    width = (q_heads + 2 * kv_heads) * head_dim
+    if parts.numel() < n_parts * rows * width:
+        raise ContractViolation("rope_kv_write_partials: parts smaller than [n, rows, W]")
+    rc = _lib.load().sp_rope_kv_write_partials(
+        parts.data_ptr(), n_parts, width, pos.data_ptr(), slot.data_ptr(), _ptr(rope),
+        _ptr(q_out), 0 if q_out is None else q_out.stride(0), k_pool.data_ptr(),
+        v_pool.data_ptr(), rows, q_heads, kv_heads, head_dim, block_size, _stream())
+    _lib.check(rc, "sp_rope_kv_write_partials")
+    _count()
+
+
 def attn_tile_tokens(q_heads: int, kv_heads: int, head_dim: int, block_size: int) -> int:
     return _lib.load().sp_attn_tile_tokens(q_heads, kv_heads, head_dim, block_size)
 

@@ -462,3 +462,38 @@ def test_gemm_partials_fused_into_rmsnorm_bitexact(M, N, K):
         assert rel(parts.sum(0), a.float() @ b.float().t()) < 1e-4
     finally:
         ops.set_gemm_workspace(None)
+
+
+def test_rope_kv_write_from_partials_bitexact():
+    """QKV projection left as K-split partials, reduced inside RoPE + KV write,
+    equals the bf16 projection (reduced by the GEMM) fed to RoPE + KV write."""
+    ops.set_gemm_workspace(torch.empty(64 << 20, dtype=torch.uint8, device="cuda"))
+    try:
+        M, hq, hk, d, bs, K = 48, 32, 8, 128, 64, 4096
+        W = (hq + 2 * hk) * d
+        a, w = rnd(M, K, seed=70), rnd(W, K, seed=71, scale=0.02)
+        n = ops.gemm_partials(M, W, K)
+        assert n > 1
+        qkv = torch.empty(M, W, device="cuda", dtype=torch.bfloat16)
+        ops.gemm(a, w, qkv, ops.EPI_STORE_BF16, M=M, N=W, K=K, lda=K, ldb=K, ldd=W)
+        parts = torch.empty(n, M, W, device="cuda")
+        ops.gemm(a, w, parts, ops.EPI_PARTIAL_F32, M=M, N=W, K=K, lda=K, ldb=K, ldd=W)
+        pos = torch.arange(M, dtype=torch.int32, device="cuda") * 3
+        slot = torch.randperm(4 * bs, device="cuda")[:M].to(torch.int32)
+        from paper_2507_11830_b200.weights import rope_table
+        tab = torch.from_numpy(rope_table(4096, d, 500000.0, None)).cuda()
+        outs = []
+        for use_parts in (False, True):
+            q = torch.empty(M, hq * d, device="cuda", dtype=torch.bfloat16)
+            kp = torch.zeros(4, hk, bs, d, device="cuda", dtype=torch.bfloat16)
+            vp = torch.zeros_like(kp)
+            kw = dict(rows=M, q_heads=hq, kv_heads=hk, head_dim=d, block_size=bs)
+            if use_parts:
+                ops.rope_kv_write_partials(parts, n, pos, slot, tab, q, kp, vp, **kw)
+            else:
+                ops.rope_kv_write(qkv, pos, slot, tab, q, kp, vp, **kw)
+            outs.append((q, kp, vp))
+        for x, y in zip(*outs):
+            assert torch.equal(x, y)
+    finally:
+        ops.set_gemm_workspace(None)
