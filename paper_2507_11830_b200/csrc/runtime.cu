@@ -1,3 +1,4 @@
+#include <algorithm>
 // Error plumbing, device check and the small HBM-bound kernels of the path:
 // embedding gather, fused residual-add + RMSNorm, RoPE + paged KV write,
 // all-to-all pack/unpack, loopback add, argmax and row gather.
@@ -86,12 +87,21 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, int64_t ldx, const flo
       t = *reinterpret_cast<const float4*>(xr + c);
       if (ar) {
         float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int s = 0; s < n_add; ++s) {  // ascending: the split-K / all-reduce order
-          const float4 b = *reinterpret_cast<const float4*>(ar + s * add_stride + c);
-          a.x += b.x;
-          a.y += b.y;
-          a.z += b.z;
-          a.w += b.w;
+        for (int s0 = 0; s0 < n_add; s0 += 4) {  // ascending: the split-K / all-reduce order
+          float4 b[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)  // loads of a batch in flight together
+            b[u] = s0 + u < n_add ? *reinterpret_cast<const float4*>(ar + (s0 + u) * add_stride + c)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (s0 + u < n_add) {
+              a.x += b[u].x;
+              a.y += b[u].y;
+              a.z += b[u].z;
+              a.w += b[u].w;
+            }
+          }
         }
         t.x += a.x;
         t.y += a.y;
@@ -378,7 +388,10 @@ extern "C" sp_status sp_add_rmsnorm(float* x, int64_t ldx, const float* add, int
     return fail(kInvalid, "add_rmsnorm: hidden and strides must be multiples of 4");
   if (rows == 0) return kOk;
   if (add && row_idx) return fail(kInvalid, "add_rmsnorm: add with row_idx unsupported");
-  const int threads = 256;
+  // one float4 per thread up to 1024 threads per row: a decode pass has few
+  // rows (one CTA each), so the row's loads must be spread wide.  A function
+  // of `hidden` only, so the reduction order is the same for every row count.
+  const int threads = std::min(1024, std::max(32, ((hidden / 4 + 31) / 32) * 32));
   const int per = (hidden + threads * 4 - 1) / (threads * 4);
   auto out = static_cast<__nv_bfloat16*>(out_bf16);
   switch (per) {
@@ -388,7 +401,7 @@ extern "C" sp_status sp_add_rmsnorm(float* x, int64_t ldx, const float* add, int
     case 4: launch_k(add_rmsnorm_kernel<4>, rows, threads, 0, S(stream), x, ldx, add, n_add, add_stride, gain, eps, row_idx, out, ldo, hidden); break;
     case 5: case 6: case 7: case 8:
       launch_k(add_rmsnorm_kernel<8>, rows, threads, 0, S(stream), x, ldx, add, n_add, add_stride, gain, eps, row_idx, out, ldo, hidden); break;
-    default: return fail(kUnsupported, "add_rmsnorm: hidden > 8192");
+    default: return fail(kUnsupported, "add_rmsnorm: hidden > 32768");
   }
   return check_launch("add_rmsnorm_kernel");
 }
