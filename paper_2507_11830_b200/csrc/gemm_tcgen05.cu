@@ -1108,7 +1108,7 @@ static int launch(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_chunk_
   return kOk;
 }
 
-// K splits of the swap-AB regime: split only until ~2/3 of the SMs stream
+// K splits of the swap-AB regime: split only until ~4/5 of the SMs stream
 // weights (all SMs when two CTAs share one), in ONE round of items — a CTA
 // with ~200 KB in flight streams well above its 1/148 share of HBM, so
 // partial SM coverage still saturates HBM, while a second round would leave a
@@ -1120,7 +1120,7 @@ static int64_t swap_splits(int N, int K, int sms) {
   const int64_t k_blocks = cdiv(K, BK);
   const int64_t n_super = cdiv(N, swp::WT * 128);
   const int64_t slots = (int64_t)sms * T::CTAS_PER_SM;
-  int64_t min_ctas = T::CTAS_PER_SM == 2 ? sms : (2 * sms) / 3;  // measured best (tools/swap_probe.py)
+  int64_t min_ctas = T::CTAS_PER_SM == 2 ? sms : (4 * sms) / 5;  // measured best in-graph (tools/decode_ablation.py)
   if (const char* e = getenv("SP_SWAP_MIN_CTAS")) min_ctas = atoi(e);
   int64_t ks = 1;
   while (n_super * ks < min_ctas && ks * 2 <= k_blocks) ++ks;
