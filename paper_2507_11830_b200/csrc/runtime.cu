@@ -78,7 +78,7 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, int64_t ldx, const flo
   float* xr = x + src_row * ldx;
   const float* ar = add ? add + (int64_t)r * hidden : nullptr;
   float v[VEC * 4];
-  float ss = 0.f;
+  float ssq[VEC];
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
     const int c = (i * blockDim.x + threadIdx.x) * 4;
@@ -114,15 +114,28 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, int64_t ldx, const flo
     v[4 * i + 1] = t.y;
     v[4 * i + 2] = t.z;
     v[4 * i + 3] = t.w;
-    ss += t.x * t.x + t.y * t.y + t.z * t.z + t.w * t.w;
+    ssq[i] = ((t.x * t.x + t.y * t.y) + t.z * t.z) + t.w * t.w;
   }
-  __shared__ float red[32];
+  // Sum of squares in an order defined on float4 CHUNKS, not threads (chunk q
+  // = i * blockDim + tid): butterfly inside each group of 32 consecutive
+  // chunks, then the group sums in ascending stride-32 order and a final
+  // butterfly — identical bits for any block size, so the launcher may pick
+  // the block size by row count.
+  __shared__ float red[256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_groups = (hidden / 4 + 31) / 32;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  for (int i = 0; i < VEC; ++i) {
+    float s = ssq[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const int grp = i * (blockDim.x >> 5) + warp;
+    if (lane == 0 && grp < n_groups) red[grp] = s;
+  }
   __syncthreads();
   if (threadIdx.x < 32) {
-    float s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    float s = 0.f;
+    for (int g = lane; g < n_groups; g += 32) s += red[g];
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (threadIdx.x == 0) red[0] = s;
@@ -388,10 +401,14 @@ extern "C" sp_status sp_add_rmsnorm(float* x, int64_t ldx, const float* add, int
     return fail(kInvalid, "add_rmsnorm: hidden and strides must be multiples of 4");
   if (rows == 0) return kOk;
   if (add && row_idx) return fail(kInvalid, "add_rmsnorm: add with row_idx unsupported");
-  // one float4 per thread up to 1024 threads per row: a decode pass has few
-  // rows (one CTA each), so the row's loads must be spread wide.  A function
-  // of `hidden` only, so the reduction order is the same for every row count.
-  const int threads = std::min(1024, std::max(32, ((hidden / 4 + 31) / 32) * 32));
+  // Few rows (a decode pass: one CTA per row) -> one float4 per thread, up to
+  // 1024 threads, so each row's loads are spread wide; many rows (prefill) ->
+  // 256-thread blocks (measured: 1024 costs ~2.5% of an 8K prefill, 256 costs
+  // ~5% of a B=64 decode).  The kernel's reduction order does not depend on
+  // the block size, so results are bit-identical either way.
+  const int wide = std::min(1024, std::max(32, ((hidden / 4 + 31) / 32) * 32));
+  int threads = rows <= 2 * 148 ? wide : std::min(wide, std::max(256, ((hidden / 32 + 31) / 32) * 32));
+  if (const char* e = getenv("SP_NORM_THREADS")) threads = atoi(e);
   const int per = (hidden + threads * 4 - 1) / (threads * 4);
   auto out = static_cast<__nv_bfloat16*>(out_bf16);
   switch (per) {

@@ -497,3 +497,23 @@ def test_rope_kv_write_from_partials_bitexact():
             assert torch.equal(x, y)
     finally:
         ops.set_gemm_workspace(None)
+
+
+@pytest.mark.parametrize("h", [256, 4096, 8192])
+def test_rmsnorm_block_size_invariant(h):
+    """add_rmsnorm picks wide blocks for few rows (decode) and 256-thread blocks
+    for many (prefill); its reduction order is defined on chunks, so a row's
+    result is bit-identical whichever block size processed it."""
+    rows = 400
+    x = torch.randn(rows, h, device="cuda") * 3
+    add = torch.randn(2, rows, h, device="cuda")
+    gain = torch.rand(h, device="cuda") + 0.5
+    big_x = x.clone()
+    big = torch.empty(rows, h, device="cuda", dtype=torch.bfloat16)
+    ops.add_rmsnorm(big_x, gain, 1e-5, big, add=add, n_add=2)  # 400 rows: narrow blocks
+    few = 37
+    small_x = x[:few].clone()
+    small = torch.empty(few, h, device="cuda", dtype=torch.bfloat16)
+    ops.add_rmsnorm(small_x, gain, 1e-5, small, add=add[:, :few].contiguous(), n_add=2)  # wide
+    assert torch.equal(small_x, big_x[:few])
+    assert torch.equal(small, big[:few])
