@@ -29,7 +29,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 from .engine import Batch, BatchItem, BatchKind, Engine, choose_mode, greedy_tokens
-from .errors import ContractViolation
+from .errors import CacheOverflow, ContractViolation
 
 
 @dataclass(frozen=True)
@@ -166,11 +166,18 @@ def run_serving(engine: Engine, trace: Sequence[TraceEntry], seed: int = 0,
     outputs: Dict[int, List[int]] = {}
     t0 = time.perf_counter()
     nxt = 0
+    pool_blocks = engine.pool.alloc.num_blocks
+    bsz = engine.pool.block_size
+    committed = 0  # blocks promised to admitted, unfinished requests
+
+    def _blocks(r: _Live) -> int:
+        return -(-(len(r.prompt) + r.entry.output_len - 1) // bsz)
 
     def now_ms() -> float:
         return (time.perf_counter() - t0) * 1e3
 
     def done(r: _Live) -> None:
+        nonlocal committed
         n = len(r.tokens)
         metrics.append(RequestMetrics(r.entry.request_id, r.entry.arrival_ms * time_scale,
                                       r.first_ms - r.entry.arrival_ms * time_scale,
@@ -179,6 +186,7 @@ def run_serving(engine: Engine, trace: Sequence[TraceEntry], seed: int = 0,
                                       len(r.prompt), n))
         outputs[r.entry.request_id] = list(r.tokens)
         engine.release(r.seq)
+        committed -= _blocks(r)
 
     while True:
         t = now_ms()
@@ -195,13 +203,25 @@ def run_serving(engine: Engine, trace: Sequence[TraceEntry], seed: int = 0,
             if wait > 0:
                 time.sleep(wait / 1e3)
             continue
+        take = []
         if queued:
-            take, budget = [], max_prefill_tokens
+            # admission: a request enters only if the paged pool can hold its whole
+            # life (prompt + outputs) next to every live request's; prompts that do
+            # not fit wait for finished requests to release their blocks
+            budget = max_prefill_tokens
             while queued and (budget is None or not take or len(queued[0].prompt) <= budget):
+                need = _blocks(queued[0])
+                if committed + need > pool_blocks:
+                    break
                 r = queued.pop(0)
+                committed += need
                 take.append(r)
                 if budget is not None:
                     budget -= len(r.prompt)
+            if not take and not decoding:
+                raise CacheOverflow(f"request {queued[0].entry.request_id} needs "
+                                    f"{_blocks(queued[0])} KV blocks, the pool has {pool_blocks}")
+        if take:
             batch = Batch(BatchKind.PREFILL, [BatchItem(r.seq, list(r.prompt)) for r in take])
             kind = "prefill"
         else:

@@ -23,19 +23,25 @@ ap.add_argument("--out", default="gpurun_out/serve")
 ap.add_argument("--tau", type=int, default=256)
 ap.add_argument("--low-rate", type=float, default=1.5)
 ap.add_argument("--burst-rate", type=float, default=25.0)
+ap.add_argument("--max-prefill-tokens", type=int, default=None)
+ap.add_argument("--kv-gb", type=float, default=None, help="paged KV pool size (default: whole trace)")
 args = ap.parse_args()
 torch.cuda.set_device(0)
 cfg = (llama31_8b if args.model == "8b" else llama33_70b)(max_seq=2048 + 256)
 trace = bursty_trace([(4000, args.low_rate), (2000, args.burst_rate)], 2048, 256, seed=11)
 w = ModelWeights.random(cfg, seed=0, world_size=1)
 blocks = len(trace) * -(-(2048 + 256) // 64) + 16
+if args.kv_gb is not None:  # memory-bound pool: the driver's admission control keeps it full
+    per_block = cfg.n_layers * 2 * cfg.kv_heads * cfg.head_dim * 2 * 64
+    blocks = int(args.kv_gb * 1e9 // per_block)
 eng = Engine(w, LoopbackGroup(1), ShiftPolicy(token_threshold=args.tau), num_blocks=blocks)
 # warm-up: capture decode graphs for the common batch sizes outside the timed trace
 warm = bursty_trace([(200, 40.0)], 128, 8, seed=1)
-run_serving(eng, warm, seed=0)
-res = run_serving(eng, trace, seed=0)
+run_serving(eng, warm, seed=0, max_prefill_tokens=args.max_prefill_tokens)
+res = run_serving(eng, trace, seed=0, max_prefill_tokens=args.max_prefill_tokens)
 s = summarize(res)
 s.update({"config": f"bursty serving, llama-{args.model} geometry, 1x B200 (configs[3] proxy)",
+          "kv_pool_blocks": blocks, "max_prefill_tokens": args.max_prefill_tokens,
           "trace": "4 s @ %.1f req/s then 2 s @ %.1f req/s, 2048-token prompts, 256 output" % (args.low_rate, args.burst_rate),
           "tau": args.tau})
 os.makedirs(args.out, exist_ok=True)
