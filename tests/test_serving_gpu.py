@@ -48,7 +48,7 @@ def test_serving_loop_prefill_first_and_shift(p):
 def test_serving_admission_waits_for_blocks():
     """A pool too small for every request at once: the driver admits requests
     only while their whole lifetime fits, the rest wait for releases; all
-    complete, the pool never overflows, and outputs equal an unconstrained run."""
+    complete with their full outputs and the pool never overflows."""
     ow = init_weights_llama(llama_tiny_config(max_seq=256), seed=0)
     trace = [TraceEntry(i, 0, 100, 30) for i in range(6)]  # 2 blocks of 64 each
     outs = []
@@ -60,6 +60,4 @@ def test_serving_admission_waits_for_blocks():
         assert eng.pool.alloc.free_blocks == blocks
         outs.append(res)
     assert max(p.n_requests for p in outs[1].passes) <= 2
-    # greedy outputs do not depend on how requests were batched (same kernels,
-    # M-invariant tiles) — checked where the pass composition is identical
     assert all(len(outs[1].outputs[i]) == 30 for i in range(6))
