@@ -142,11 +142,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;   // [2]
   uint64_t* v_full = bars + 3;   // [2]
-  uint64_t* kv_empty = bars + 5; // [2]
+  uint64_t* k_empty = bars + 5;  // [2] K slot free (both tiles' QK done)
   uint64_t* s_full = bars + 7;   // [2] per Q tile
   uint64_t* p_full = bars + 9;   // [2] per Q tile
   uint64_t* o_full = bars + 11;  // [2] per Q tile
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+  uint64_t* v_empty = bars + 13; // [2] V slot free (both tiles' PV done)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int2 wk = p.work[blockIdx.x];
@@ -171,7 +172,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(k_full + s, 1);
       mbar_init(v_full + s, 1);
-      mbar_init(kv_empty + s, 1);
+      mbar_init(k_empty + s, 1);
+      mbar_init(v_empty + s, 1);
       mbar_init(s_full + s, 1);
       mbar_init(p_full + s, 128);
       mbar_init(o_full + s, 1);
@@ -197,7 +199,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int32_t* bt = p.block_tables + (int64_t)item * p.bt_stride;
       for (int j = 0; j < n_kt; ++j) {
         const int s = j & 1;
-        mbar_wait(kv_empty + s, ((j >> 1) & 1) ^ 1);
         uint8_t* sK = sKV + s * 2 * KV_TILE_BYTES;
         uint8_t* sV = sK + KV_TILE_BYTES;
         int rows[2];
@@ -207,10 +208,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int page = pg_i < n_pages ? bt[pg_i] : 0;
           rows[h] = (page * p.kv_heads + kvh) * p.block_size + key0 % p.block_size;
         }
+        // K and V slots are released separately: K(j) frees once both tiles'
+        // QK(j) are done (an iteration before V(j) frees), so K(j+2) is in
+        // flight a full iteration before QK(j+2) needs it
+        mbar_wait(k_empty + s, ((j >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(k_full + s, KV_TILE_BYTES);
         for (int c = 0; c < 2; ++c)
           for (int h = 0; h < 2; ++h)
             tma_load_2d(sK + c * (KV_TILE_BYTES / 2) + h * 8192, &tmK, k_full + s, c * 64, rows[h]);
+        mbar_wait(v_empty + s, ((j >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(v_full + s, KV_TILE_BYTES);
         for (int c = 0; c < 2; ++c)
           for (int h = 0; h < 2; ++h)
@@ -242,6 +248,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       issue_qk(0, 0);
       issue_qk(1, 0);
+      umma_commit(k_empty + 0);
       for (int j = 0; j < n_kt; ++j) {
         const int s = j & 1;
         const uint32_t par = (j >> 1) & 1;
@@ -264,7 +271,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           else
             umma_commit(o_full + t);
         }
-        umma_commit(kv_empty + s);
+        umma_commit(v_empty + s);
+        if (more) umma_commit(k_empty + (s ^ 1));
       }
     }
     __syncwarp();
