@@ -30,16 +30,15 @@ namespace attn_tc {
 constexpr int HD = 128;
 constexpr int QROWS = 128;       // rows per Q tile
 constexpr int KT = 128;          // keys per tile
-// Two measured-negative softmax variants kept as build knobs (tools/kbench.py attn,
-// 8K causal): one MUFU.EX2.bf16x2 per pair (1023 vs 1051 TFLOP/s) and an
-// FMA-pipe polynomial for part of the pairs (1-4% slower).  ncu shows the SFU
-// at ~54% and the softmax warps mostly waiting for S: the ping-pong schedule,
-// not the exponential, bounds this kernel.
+// Softmax exponential variants (tools/kbench.py attn, 8K causal, after the K/V
+// release split): 4 of every 32 pairs through the FMA-pipe polynomial
+// (ATTN_POLY_PAIRS=4) measured best, 1190 vs 1140 TFLOP/s all-MUFU (8: 1178,
+// 16: 1114); one MUFU.EX2.bf16x2 per pair (ATTN_EXP_BF16X2=1) was slower (1077).
 #ifndef ATTN_EXP_BF16X2
 #define ATTN_EXP_BF16X2 0
 #endif
 #ifndef ATTN_POLY_PAIRS
-#define ATTN_POLY_PAIRS 0
+#define ATTN_POLY_PAIRS 4
 #endif
 constexpr int kPolyPairs = ATTN_POLY_PAIRS;  // of 32 pairs per 64 columns (tools/kbench.py attn)
 
