@@ -210,7 +210,8 @@ class _GraphEntry:
 class Engine:
     def __init__(self, weights: ModelWeights, group: DeviceGroup, policy: ShiftPolicy,
                  swiftkv: Optional[SwiftKvConfig] = None, *, num_blocks: Optional[int] = None,
-                 block_size: int = 64, cuda_graphs: bool = True, max_pass_tokens: int = 16384):
+                 block_size: int = 64, cuda_graphs: bool = True, max_pass_tokens: int = 16384,
+                 sp_degree: Optional[int] = None):
         cfg = weights.config
         self.weights = weights
         self.config: ModelConfig = cfg
@@ -221,6 +222,17 @@ class Engine:
         if weights.world_size != self.world_size:
             raise ConfigError("weights were laid out for a different world size")
         cfg.check_world(self.world_size)
+        # SP mode runs SP(s) x TP(P/s) when sp_degree = s < P (the paper's
+        # "SP x TP = P" base config); s = P is the reference's pure SP
+        self.sp_degree = self.world_size if sp_degree is None else sp_degree
+        if self.sp_degree < 1 or self.world_size % self.sp_degree:
+            raise ConfigError("sp_degree must divide the world size")
+        if self.sp_degree < self.world_size:
+            t = self.world_size // self.sp_degree
+            if cfg.ffn_dim // t % 128 or cfg.kv_heads % self.world_size:
+                raise ConfigError("SP x TP needs 128-row SwiGLU shards and P | kv_heads")
+            s = self.sp_degree
+            group.make_subgroups([[g * s + i for g in range(t)] for i in range(s)])
         self.partition = partition_heads(cfg.n_heads, self.world_size)
         self.kv_partition = partition_heads(cfg.kv_heads, self.world_size)
         self.device = weights.embed.device
@@ -308,6 +320,7 @@ class Engine:
         graph_key = None
         if (self.cuda_graphs and cut is None and not span_logits
                 and not getattr(self.group, "_stage", False)  # host-staged collectives
+                and not (mode is ParallelMode.SP and self.sp_degree < self.world_size)
                 and all(len(it.tokens) == 1 for it in batch.items)):
             graph_key = (mode, len(batch.items), self._bt_width_cap(batch))
         shape = self.pass_shape(batch, span_logits) if graph_key else None
@@ -456,8 +469,10 @@ class Engine:
             wl = [(i, t0, hist[i] + t0) for i in range(n) for t0 in range(0, spans[i], tt)]
             wl.sort(key=lambda w: -w[2])  # heaviest causal tiles first
             work = np.asarray([(i, t0) for i, t0, _ in wl], dtype=np.int32).reshape(-1, 2)
-        bounds = shard_bounds(M, P)
-        # SP: per-rank local indices of the rows whose logits are returned
+        # SP token shards: P of them, or s under SP(s) x TP(P/s)
+        n_shards = self.sp_degree if mode is ParallelMode.SP else P
+        bounds = shard_bounds(M, n_shards)
+        # SP: per-shard local indices of the rows whose logits are returned
         sp_rows = []
         for lo, hi in bounds:
             if span_logits:
@@ -470,7 +485,7 @@ class Engine:
         parts = dict(toks=toks, pos=pos, slots=slots, cu=cu, first=first, kvlen=kvlen,
                      bt=bt.reshape(-1), ends=ends, work=work.reshape(-1),
                      tail_pos=tail_pos, tail_slot=tail_slot, tail_cu=tail_cu)
-        for r in range(P):
+        for r in range(n_shards):
             parts[f"sprows{r}"] = sp_rows[r]
         # every array starts on a 16-byte boundary (the kernels read int2 pairs)
         total = sum(-(-a.size // 4) * 4 for a in parts.values())
@@ -826,6 +841,10 @@ class Engine:
 
     # ================================================================= SP
     def _forward_sp(self, meta, batch, meters, span_logits, cut):
+        if self.sp_degree < self.world_size:
+            if cut is not None:
+                raise ContractViolation("SwiftKV early exit is implemented for pure SP/TP only")
+            return self._forward_sptp(meta, batch, meters, span_logits)
         cfg, w, g = self.config, self.weights, self.group
         P = self.world_size
         M, h, d = meta.M, cfg.hidden, cfg.head_dim
@@ -952,6 +971,129 @@ class Engine:
             parts[r] = lg
         logits = g.all_gather_rows(parts, meta.sp_counts) if P > 1 else parts[0]
         return self._split(logits, meta, span_logits)
+
+    def _forward_sptp(self, meta, batch, meters, span_logits):
+        """SP(s) x TP(t), P = s*t.  Rank r = g*s + i: TP group g (heads of
+        ranks g*s .. g*s+s-1, ffn shard g), token shard i.  Per layer: QKV on
+        shard i with group g's weight rows, seq->head all-to-all inside the SP
+        group {g*s+i'} (rank r ends with head block r — the TP(P)/SP(P) KV
+        layout, so the cache stays mode-invariant), attention, head->seq
+        all-to-all back, O and MLP as TP(t) partials all-reduced inside the TP
+        group {g'*s+i}.  Not in the reference (SPEC.md:334 leaves mixed modes
+        unimplemented); parity is checked against the dense oracle and the pure
+        modes."""
+        cfg, w, grp = self.config, self.weights, self.group
+        P, s = self.world_size, self.sp_degree
+        t = P // s
+        M, h, d = meta.M, cfg.hidden, cfg.head_dim
+        W = w.qkv_width                  # q|k|v width of ONE rank's head block
+        hqw = cfg.n_heads // P * d       # one rank's q width
+        fl = cfg.ffn_dim // t            # this TP group's ffn shard
+        dev, eps = self.device, cfg.norm_eps
+        rows, bounds = meta.rows, meta.bounds   # per token shard i
+        grp_of = {r: (r // s, r % s) for r in range(P)}
+        xs = {}
+        for r in grp.local_ranks:
+            g, i = grp_of[r]
+            lo, hi = bounds[i]
+            xs[r] = torch.empty((hi - lo, h), dtype=torch.float32, device=dev)
+            ops.embed(meta.toks[lo:hi], w.embed, xs[r], meta.pos[lo:hi], w.pos_table)
+        # split tables: exchanges stay inside SP groups (zero rows elsewhere)
+        in_fwd = {r: [rows[r % s] if d2 // s == r // s else 0 for d2 in range(P)] for r in range(P)}
+        out_fwd = {r: [rows[s2 % s] if s2 // s == r // s else 0 for s2 in range(P)] for r in range(P)}
+        in_back = {r: [rows[d2 % s] if d2 // s == r // s else 0 for d2 in range(P)] for r in range(P)}
+        out_back = {r: [rows[r % s] if s2 // s == r // s else 0 for s2 in range(P)] for r in range(P)}
+        tp_members = {r: [g2 * s + r % s for g2 in range(t)] for r in range(P)}
+        pending = None
+        for layer in range(cfg.n_layers):
+            lw = w.layers[layer]
+            send, recv = {}, {}
+            for r in grp.local_ranks:
+                g, i = grp_of[r]
+                xn = torch.empty((rows[i], h), dtype=torch.bfloat16, device=dev)
+                ops.add_rmsnorm(xs[r], lw.attn_gain, eps, xn,
+                                add=None if pending is None else pending[r])
+                # group g's s head blocks; block i' -> send block i' (fused pack)
+                send[r] = torch.empty((s * rows[i], W), dtype=torch.bfloat16, device=dev)
+                ops.gemm(xn, lw.wqkv[g * s * W:(g + 1) * s * W], send[r], ops.EPI_STORE_BF16,
+                         M=rows[i], N=s * W, K=h, lda=h, ldb=h, ldd=W, peer_width=W,
+                         peer_stride=rows[i] * W, meter=meters[r])
+                recv[r] = torch.empty((M, W), dtype=torch.bfloat16, device=dev)
+            grp.all_to_all(send, recv, in_fwd, out_fwd, row_bytes=W * 2, group_size=s)
+            self._stage_all(layer, batch)
+            att = {}
+            for r in grp.local_ranks:
+                q = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
+                self._kv_write(r, layer, recv[r], q, meta, batch)
+                o = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
+                self._attend(r, layer, q, o, meta, meters[r])
+                att[r] = o
+            back = {r: torch.empty((s * rows[r % s], hqw), dtype=torch.bfloat16, device=dev)
+                    for r in grp.local_ranks}
+            grp.all_to_all(att, back, in_back, out_back, row_bytes=hqw * 2, group_size=s)
+            parts = {}
+            for r in grp.local_ranks:
+                g, i = grp_of[r]
+                part = torch.empty((rows[i], h), dtype=torch.float32, device=dev)
+                # A = [s blocks][rows_i][hqw] (the receive layout), K = s * hqw
+                ops.gemm(back[r], lw.wo[:, g * s * hqw:], part, ops.EPI_STORE_F32, M=rows[i],
+                         N=h, K=s * hqw, lda=hqw, ldb=cfg.n_heads * d, ldd=h,
+                         a_kchunk=hqw if hqw % 64 == 0 and s > 1 else 0,
+                         a_chunk_stride=rows[i] * hqw, meter=meters[r])
+                parts[r] = part
+            red = self._group_sum(parts, tp_members)
+            parts = {}
+            for r in grp.local_ranks:
+                g, i = grp_of[r]
+                xn2 = torch.empty((rows[i], h), dtype=torch.bfloat16, device=dev)
+                ops.add_rmsnorm(xs[r], lw.mlp_gain, eps, xn2, add=red[r])
+                act = torch.empty((rows[i], fl), dtype=torch.bfloat16, device=dev)
+                if cfg.mlp == "swiglu":
+                    ops.gemm(xn2, lw.wgu[g * 2 * fl:(g + 1) * 2 * fl], act, ops.EPI_SWIGLU,
+                             M=rows[i], N=2 * fl, K=h, lda=h, ldb=h, ldd=fl, meter=meters[r])
+                else:
+                    ops.gemm(xn2, lw.wgu[g * fl:(g + 1) * fl], act, ops.EPI_GELU, M=rows[i],
+                             N=fl, K=h, lda=h, ldb=h, ldd=fl, meter=meters[r])
+                part = torch.empty((rows[i], h), dtype=torch.float32, device=dev)
+                ops.gemm(act, lw.wdown[:, g * fl:], part, ops.EPI_STORE_F32, M=rows[i], N=h,
+                         K=fl, lda=fl, ldb=cfg.ffn_dim, ldd=h, meter=meters[r])
+                parts[r] = part
+            pending = self._group_sum(parts, tp_members)
+        # final norm + LM head on each shard's returned rows; every TP group holds
+        # the same rows, so group 0's shards are gathered (in shard order)
+        lg_parts = {}
+        counts = [0] * P
+        for r in grp.local_ranks:
+            g, i = grp_of[r]
+            cnt = meta.sp_counts[i]
+            ops.add_f32(xs[r], pending[r], xs[r])
+            xf = torch.empty((cnt, h), dtype=torch.bfloat16, device=dev)
+            ops.add_rmsnorm(xs[r], w.final_gain, eps, xf, row_idx=getattr(meta, f"sprows{i}"),
+                            rows=cnt)
+            lg = torch.empty((cnt, cfg.vocab_size), dtype=torch.float32, device=dev)
+            ops.gemm(xf, w.head, lg, ops.EPI_STORE_F32, M=cnt, N=cfg.vocab_size, K=h, lda=h,
+                     ldb=h, ldd=cfg.vocab_size, meter=meters[r])
+            lg_parts[r] = lg
+        for r in range(P):
+            counts[r] = meta.sp_counts[r % s] if r // s == 0 else 0
+        for r in grp.local_ranks:  # ranks outside group 0 contribute nothing
+            if r // s:
+                lg_parts[r] = lg_parts[r][:0]
+        logits = grp.all_gather_rows(lg_parts, counts) if P > 1 else lg_parts[0]
+        return self._split(logits, meta, span_logits)
+
+    def _group_sum(self, parts: Dict[int, torch.Tensor], members: Dict[int, List[int]]):
+        """TP all-reduce inside each TP group of SP x TP (one call per group)."""
+        out: Dict[int, torch.Tensor] = {}
+        done = set()
+        for r in sorted(members):
+            key = tuple(members[r])
+            if key in done or not any(m in parts for m in key):
+                continue
+            done.add(key)
+            out.update(self.group.all_reduce_sum_group({m: parts[m] for m in key if m in parts},
+                                                       list(key)))
+        return out
 
     def _mlp_up_full(self, xn2, lw, act, rows, meter):
         cfg = self.config

@@ -72,12 +72,24 @@ class DeviceGroup(_Ledger):
     local_ranks: List[int]
     device: torch.device
 
-    # byte accounting from the global split tables (every rank knows them)
-    def _charge_a2a(self, in_splits: Dict[int, List[int]], row_bytes: int) -> None:
+    # byte accounting from the global split tables (every rank knows them);
+    # group_size: the exchange runs inside groups of that size (SP x TP)
+    def _charge_a2a(self, in_splits: Dict[int, List[int]], row_bytes: int,
+                    group_size: Optional[int] = None) -> None:
         p = self.world_size
-        self.charge("all_to_all", [(p - 1) / p * sum(in_splits[r]) * row_bytes for r in range(p)])
+        g = p if group_size is None else group_size
+        self.charge("all_to_all", [(g - 1) / g * sum(in_splits[r]) * row_bytes for r in range(p)])
 
-    def all_to_all(self, send, recv, in_splits, out_splits, row_bytes):  # pragma: no cover
+    def make_subgroups(self, groups: Sequence[Sequence[int]]) -> None:
+        """Declare the rank groups all_reduce_sum_group will be called with
+        (collective across processes: every rank declares every group)."""
+
+    def all_reduce_sum_group(self, parts: Dict[int, torch.Tensor],
+                             members: Sequence[int]) -> Dict[int, torch.Tensor]:  # pragma: no cover
+        raise NotImplementedError
+
+    def all_to_all(self, send, recv, in_splits, out_splits, row_bytes,
+                   group_size=None):  # pragma: no cover
         raise NotImplementedError
 
     def all_reduce_sum(self, parts: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:  # pragma: no cover
@@ -103,7 +115,7 @@ class LoopbackGroup(DeviceGroup):
 
     def all_to_all(self, send: Dict[int, torch.Tensor], recv: Dict[int, torch.Tensor],
                    in_splits: Dict[int, List[int]], out_splits: Dict[int, List[int]],
-                   row_bytes: int) -> None:
+                   row_bytes: int, group_size: Optional[int] = None) -> None:
         """Rank r sends rows in_splits[r][s] of send[r] (in peer order) to s;
         rank s receives them at recv[s] in source order (fabric.py:145-171)."""
         p = self.world_size
@@ -117,7 +129,7 @@ class LoopbackGroup(DeviceGroup):
                 if n:
                     recv[s][off:off + n].copy_(send[r][offs_in[r][s]:offs_in[r][s] + n])
                 off += n
-        self._charge_a2a(in_splits, row_bytes)
+        self._charge_a2a(in_splits, row_bytes, group_size)
 
     def all_reduce_sum(self, parts: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:
         """Ascending-rank f32 sum; every rank gets the same (aliased) result."""
@@ -131,6 +143,21 @@ class LoopbackGroup(DeviceGroup):
                 self._add(total, parts[r], total)
         self.charge("all_reduce", [2.0 * (p - 1) / p * parts[0].numel() * parts[0].element_size()] * p)
         return {r: total for r in range(p)}
+
+    def all_reduce_sum_group(self, parts: Dict[int, torch.Tensor],
+                             members: Sequence[int]) -> Dict[int, torch.Tensor]:
+        """all_reduce_sum among `members` only (the TP groups of SP x TP):
+        ascending-member f32 sum, aliased to every member."""
+        members = sorted(members)
+        g = len(members)
+        total = parts[members[0]]
+        if g > 1:
+            total = total.clone()
+            for r in members[1:]:
+                self._add(total, parts[r], total)
+        nb = 2.0 * (g - 1) / g * total.numel() * total.element_size()
+        self.charge("all_reduce", [nb if r in members else 0.0 for r in range(self.world_size)])
+        return {r: total for r in members}
 
     def all_gather_rows(self, parts: Dict[int, torch.Tensor], counts: List[int]) -> torch.Tensor:
         p = self.world_size
@@ -157,7 +184,7 @@ class NcclGroup(DeviceGroup):
         # several ranks on ONE GPU in tests; B200 runs use NCCL directly)
         self._stage = dist.get_backend() == "gloo" and self.device.type == "cuda"
 
-    def all_to_all(self, send, recv, in_splits, out_splits, row_bytes) -> None:
+    def all_to_all(self, send, recv, in_splits, out_splits, row_bytes, group_size=None) -> None:
         me = self.rank
         if self.world_size > 1:
             if self._stage:
@@ -171,7 +198,7 @@ class NcclGroup(DeviceGroup):
             else:
                 self._dist.all_to_all_single(recv[me], send[me], output_split_sizes=out_splits[me],
                                              input_split_sizes=in_splits[me])
-        self._charge_a2a(in_splits, row_bytes)
+        self._charge_a2a(in_splits, row_bytes, group_size)
 
     def all_reduce_sum(self, parts):
         me, p = self.rank, self.world_size
@@ -184,6 +211,30 @@ class NcclGroup(DeviceGroup):
             else:
                 self._dist.all_reduce(t)
         self.charge("all_reduce", [2.0 * (p - 1) / p * t.numel() * t.element_size()] * p)
+        return {me: t}
+
+    def make_subgroups(self, groups) -> None:
+        self._sub = getattr(self, "_sub", {})
+        for members in groups:
+            key = tuple(sorted(members))
+            if key not in self._sub:  # new_group is collective: same order on every rank
+                self._sub[key] = self._dist.new_group(list(key))
+
+    def all_reduce_sum_group(self, parts, members):
+        me = self.rank
+        key = tuple(sorted(members))
+        t = parts[me]
+        g = len(key)
+        if g > 1:
+            grp = self._sub[key]
+            if self._stage:
+                h = t.cpu()
+                self._dist.all_reduce(h, group=grp)
+                t.copy_(h)
+            else:
+                self._dist.all_reduce(t, group=grp)
+        nb = 2.0 * (g - 1) / g * t.numel() * t.element_size()
+        self.charge("all_reduce", [nb if r in key else 0.0 for r in range(self.world_size)])
         return {me: t}
 
     def all_gather_rows(self, parts, counts) -> torch.Tensor:
