@@ -200,6 +200,13 @@ sp_status sp_peer_allreduce_add_rmsnorm(const unsigned long long* part_ptrs, int
  * In-process (loopback) all-reduce: dst = a + b, f32, ascending order as in
  * DeviceGroup.all_reduce_sum (fabric.py:117-143).
  */
+/* Cross-process peer buffers (CUDA IPC) for the fused exchanges when ranks are
+ * separate processes: export the allocation holding `ptr` as a 64-byte handle
+ * plus the offset of `ptr` inside it; import a peer's handle (mapped over
+ * NVLink P2P when the peer is another GPU). */
+sp_status sp_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out);
+sp_status sp_ipc_import(const void* handle, int64_t offset, void** ptr_out);
+
 sp_status sp_add_f32(const float* a, const float* b, float* dst, int64_t n, void* stream);
 /* greedy_token (model.py:303-307): per row argmax, lowest index wins ties. */
 sp_status sp_argmax(const float* logits, int64_t ld, int rows, int vocab, int32_t* idx,

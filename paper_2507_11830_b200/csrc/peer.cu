@@ -7,6 +7,10 @@
 // all P flags and resets them (reset-on-consume keeps the protocol valid under
 // CUDA-graph replay; the SP data dependences order the next signal after the
 // reset).  In-process (loopback) ranks use the same kernels on one GPU.
+#include <cuda.h>
+#include <cstring>
+#include <string>
+
 #include "../../include/shiftpar.h"
 #include "common.cuh"
 
@@ -192,4 +196,45 @@ extern "C" sp_status sp_peer_wait(int* flags, int peers, void* stream) {
   launch_k(peer_wait_kernel, 1, 32 * ((peers + 31) / 32), 0, reinterpret_cast<cudaStream_t>(stream),
            flags, peers);
   return check_launch("peer_wait_kernel");
+}
+
+// ------------------------------------------------------------------ CUDA IPC
+// Cross-process peer buffers (one process per GPU under torchrun): export the
+// allocation holding `ptr` (offset kept separately, since the caching
+// allocator hands out interior pointers), import a peer's, close an import.
+typedef CUresult (*PFN_memGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+extern "C" sp_status sp_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out) {
+  if (!ptr || !handle_out || !offset_out) return fail(kInvalid, "ipc_export: null argument");
+  static PFN_memGetAddressRange range = nullptr;
+  if (!range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        !fn)
+      return fail(kCuda, "cuMemGetAddressRange entry point unavailable");
+    range = reinterpret_cast<PFN_memGetAddressRange>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+    return fail(kCuda, "ipc_export: cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return fail(kCuda, std::string("ipc_export: ") + cudaGetErrorString(e));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle_out, &h, sizeof(h));
+  *offset_out = reinterpret_cast<uintptr_t>(ptr) - static_cast<uintptr_t>(base);
+  return kOk;
+}
+
+extern "C" sp_status sp_ipc_import(const void* handle, int64_t offset, void** ptr_out) {
+  if (!handle || !ptr_out || offset < 0) return fail(kInvalid, "ipc_import: bad argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(kCuda, std::string("ipc_import: ") + cudaGetErrorString(e));
+  *ptr_out = static_cast<uint8_t*>(base) + offset;
+  return kOk;
 }

@@ -253,8 +253,12 @@ class Engine:
         self._peer: Optional[PeerLinks] = None
         if fused_a2a_enabled(group):
             hqw = cfg.n_heads // self.world_size * cfg.head_dim
-            self._peer = PeerLinks(group, max_pass_tokens, weights.qkv_width, hqw, cfg.hidden,
-                                   self.device)
+            try:
+                self._peer = PeerLinks(group, max_pass_tokens, weights.qkv_width, hqw, cfg.hidden,
+                                       self.device)
+            except Exception as e:  # e.g. no IPC/P2P between the ranks' GPUs
+                warnings.warn(f"peer-memory exchanges unavailable ({e}); using collectives")
+                self._peer = None
         self.mode_log: List[ParallelMode] = []
         self.step_records: List[StepRecord] = []
         self._step_counter = 0

@@ -198,6 +198,22 @@ def embed(ids: torch.Tensor, table: torch.Tensor, out: torch.Tensor,
     _count()
 
 
+def ipc_export(t: torch.Tensor) -> tuple:
+    """(64-byte CUDA IPC handle of the allocation holding t, offset of t in it)."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64(0)
+    _lib.check(_lib.load().sp_ipc_export(t.data_ptr(), h, ctypes.byref(off)), "sp_ipc_export")
+    return h.raw, off.value
+
+
+def ipc_import(handle: bytes, offset: int) -> int:
+    """Device address (in this process) of a peer's exported buffer."""
+    ptr = ctypes.c_void_p(0)
+    _lib.check(_lib.load().sp_ipc_import(ctypes.create_string_buffer(handle, 64), offset,
+                                         ctypes.byref(ptr)), "sp_ipc_import")
+    return int(ptr.value)
+
+
 def gemm_partials(M: int, N: int, K: int) -> int:
     """How many f32 [M, N] partial slabs an EPI_PARTIAL_F32 GEMM writes."""
     return int(_lib.load().sp_gemm_partials(M, N, K))

@@ -8,9 +8,10 @@ Each rank owns, at addresses every peer knows:
 
 Device tables of the P peers' addresses feed the kernels (sp_gemm_bf16_to_peers,
 sp_peer_scatter_rows, sp_peer_signal).  In-process ranks (LoopbackGroup) use
-plain buffers on the one device; across GPUs the buffers live in one
-torch symmetric-memory allocation per rank whose peer mappings are NVLink
-addresses (opt-in with SP_FUSED_A2A=1 until validated on a multi-GPU box).
+plain buffers on the one device; across processes each rank's buffer is
+exported by CUDA IPC and mapped by every peer (NVLink P2P between GPUs; the
+multi-process tests run several ranks on one GPU, bit-identical to the
+in-process path).  On by default; SP_FUSED_A2A=0 selects the NCCL collectives.
 """
 
 from __future__ import annotations
@@ -57,15 +58,15 @@ class PeerLinks:
                 self._bufs[r] = buf
                 bases[r] = buf.data_ptr()
                 self._views(r, buf)
-        else:  # one symmetric allocation per rank; peers map it over NVLink
+        else:  # one buffer per rank process; peers map it by CUDA IPC (NVLink P2P)
             import torch.distributed as dist
-            import torch.distributed._symmetric_memory as symm_mem
-            buf = symm_mem.empty(total, dtype=torch.uint8, device=device)
-            buf.zero_()
-            hdl = symm_mem.rendezvous(buf, dist.group.WORLD.group_name)
+            from . import ops
+            buf = torch.zeros(total, dtype=torch.uint8, device=device)
+            handles: List = [None] * P
+            dist.all_gather_object(handles, ops.ipc_export(buf))
+            for r in range(P):
+                bases[r] = buf.data_ptr() if r == group.rank else ops.ipc_import(*handles[r])
             self._bufs = {group.rank: buf}
-            self._hdl = hdl
-            bases = list(hdl.buffer_ptrs)
             self._views(group.rank, buf)
             torch.cuda.synchronize()
             dist.barrier()
@@ -99,7 +100,4 @@ class PeerLinks:
 def fused_a2a_enabled(group: DeviceGroup) -> bool:
     if group.world_size < 2:
         return False
-    env = os.environ.get("SP_FUSED_A2A")
-    if isinstance(group, LoopbackGroup):
-        return env != "0"
-    return env == "1"
+    return os.environ.get("SP_FUSED_A2A") != "0"

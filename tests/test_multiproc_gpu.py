@@ -91,12 +91,18 @@ def _worker(rank, world, port, q, sp_degree=None):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,sp_degree", [(2, None), (4, 2)])
-def test_multi_process_engine_matches_loopback(world, sp_degree):
+@pytest.mark.parametrize("world,sp_degree,fused", [(2, None, False), (4, 2, False),
+                                                   (2, None, True), (4, None, True)])
+def test_multi_process_engine_matches_loopback(world, sp_degree, fused, monkeypatch):
     """(2, None): pure SP/TP over two processes, bit-identical; (4, 2): the
     SP(2) x TP(2) base config over four processes (TP-group all-reduces on
     sub-groups), bit-identical for the mixed prefill, within bf16 tolerance
-    for the TP(4) decodes (four-way sums in gloo's order)."""
+    for the TP(4) decodes (four-way sums in gloo's order).  fused: the SP
+    all-to-alls and TP all-reduces go over CUDA-IPC-mapped peer buffers
+    (GEMM epilogue stores into peers, release/acquire flags, one-shot
+    ascending-rank all-reduce in the norm kernel) — concurrently running
+    processes, bit-identical to the in-process fused path at any P."""
+    monkeypatch.setenv("SP_FUSED_A2A", "1" if fused else "0")
     import torch.multiprocessing as mp
     from paper_2507_11830_b200 import Engine, LoopbackGroup, ShiftPolicy
 
@@ -125,7 +131,7 @@ def test_multi_process_engine_matches_loopback(world, sp_degree):
         assert len(got) == len(want)
         for k, (g, w) in enumerate(zip(got, want)):
             g = np.asarray(g, dtype=np.float32)
-            if world == 2 or k == 0:
+            if world == 2 or k == 0 or fused:
                 # two-member sums (P = 2, and the TP(2) groups of the mixed
                 # prefill) leave no reduction-order freedom: bit-identical
                 assert np.array_equal(g, w), (r, k)
