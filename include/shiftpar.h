@@ -148,6 +148,24 @@ sp_status sp_attention(const void* q, int64_t ldq, int64_t q_rows, const void* k
                        const int32_t* work, int n_work, int max_q_len, int max_kv_len,
                        void* out, int64_t ldo, int q_heads, int kv_heads, int head_dim,
                        int block_size, void* ws, int64_t ws_bytes, void* stream);
+/* Split-KV variant of the tcgen05 prefill (head_dim 128) for passes with few
+ * work tiles (e.g. one long request under SP=8: 128 CTAs, causal rows up to
+ * 64x longer than others).  Entry w of `work` (item, t0) comes with
+ * split[w] = (first key tile, end key tile, slot, 0): slot < 0 -> the entry
+ * covers all of its keys and stores the output; slot >= 0 -> unnormalised
+ * partial O and (max, sum) go to workspace slot `slot * kv_heads + kv_head`
+ * ([slots][256][128] f32 then [slots][256][2] f32, slots = ws_bytes /
+ * (256*130*4)), and combine entry (item, t0, first slot, n slots) merges them
+ * in ascending key order (deterministic). */
+sp_status sp_attention_prefill_split(const void* q, int64_t ldq, int64_t q_rows,
+                                     const void* k_pool, const void* v_pool, int64_t pool_blocks,
+                                     const int32_t* block_tables, int64_t bt_stride,
+                                     const int32_t* cu_q, const int32_t* first_pos,
+                                     const int32_t* kv_len, const int32_t* work,
+                                     const int32_t* split, int n_work, const int32_t* combine,
+                                     int n_combine, void* out, int64_t ldo, int q_heads,
+                                     int kv_heads, int head_dim, int block_size, void* ws,
+                                     int64_t ws_bytes, void* stream);
 int64_t sp_attn_workspace_bytes(int n_items, int q_heads, int head_dim, int max_kv_len);
 /* Tokens per prefill work tile (host schedule).  head_dim 128 with pages of a
  * multiple of 64 keys selects the tcgen05/TMEM kernel (2 x 128 packed rows

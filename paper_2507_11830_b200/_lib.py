@@ -41,6 +41,9 @@ SIGNATURES = {
                                 _vp]),
     "sp_gemm_partials": (_c_int, [_c_int, _c_int, _c_int]),
     "sp_ipc_export": (_c_int, [_vp, _vp, ctypes.POINTER(_i64)]),
+    "sp_attention_prefill_split": (_c_int, [_vp, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp,
+                                            _vp, _vp, _vp, _c_int, _vp, _c_int, _vp, _i64, _c_int,
+                                            _c_int, _c_int, _c_int, _vp, _i64, _vp]),
     "sp_ipc_import": (_c_int, [_vp, _i64, ctypes.POINTER(_vp)]),
     "sp_rope_kv_write_partials": (_c_int, [_vp, _c_int, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp,
                                            _c_int, _c_int, _c_int, _c_int, _c_int, _vp]),

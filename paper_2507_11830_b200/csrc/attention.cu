@@ -656,7 +656,9 @@ int launch_prefill_tc(const void* q, int64_t ldq, int64_t q_rows_total, const vo
                       const void* v_pool, int64_t pool_rows, const int32_t* block_tables,
                       int64_t bt_stride, const int32_t* cu_q, const int32_t* first_pos,
                       const int32_t* kv_len, const int32_t* work, int n_work, void* out,
-                      int64_t ldo, int q_heads, int kv_heads, int block_size, cudaStream_t st);
+                      int64_t ldo, int q_heads, int kv_heads, int block_size, cudaStream_t st,
+                      const int32_t* split = nullptr, const int32_t* combine = nullptr,
+                      int n_combine = 0, void* ws = nullptr, int64_t ws_bytes = 0);
 }
 
 using namespace sp;
@@ -679,6 +681,27 @@ extern "C" int64_t sp_attn_workspace_bytes(int n_items, int q_heads, int head_di
   (void)max_kv_len;
   const int64_t splits = 64;
   return (int64_t)n_items * q_heads * splits * (head_dim + 1) * 4;
+}
+
+extern "C" sp_status sp_attention_prefill_split(
+    const void* q, int64_t ldq, int64_t q_rows, const void* k_pool, const void* v_pool,
+    int64_t pool_blocks, const int32_t* block_tables, int64_t bt_stride, const int32_t* cu_q,
+    const int32_t* first_pos, const int32_t* kv_len, const int32_t* work, const int32_t* split,
+    int n_work, const int32_t* combine, int n_combine, void* out, int64_t ldo, int q_heads,
+    int kv_heads, int head_dim, int block_size, void* ws, int64_t ws_bytes, void* stream) {
+  if (n_work <= 0 || n_combine < 0 || !work || !split || (n_combine > 0 && !combine))
+    return fail(kInvalid, "attention split: bad work lists");
+  if (kv_heads <= 0 || q_heads % kv_heads) return fail(kInvalid, "attention: q_heads % kv_heads != 0");
+  if (!use_tc_prefill(q_heads, kv_heads, head_dim, block_size))
+    return fail(kUnsupported, "attention split: needs the tcgen05 prefill path (head_dim 128)");
+  if (ldq % 8 || ldo % 8 || q_rows <= 0 || pool_blocks <= 0)
+    return fail(kInvalid, "attention: tcgen05 prefill needs 16-byte rows and sizes");
+  if (!ws || ws_bytes <= 0) return fail(kInvalid, "attention split: workspace required");
+  return launch_prefill_tc(q, ldq, q_rows, k_pool, v_pool,
+                           pool_blocks * (int64_t)kv_heads * block_size, block_tables, bt_stride,
+                           cu_q, first_pos, kv_len, work, n_work, out, ldo, q_heads, kv_heads,
+                           block_size, reinterpret_cast<cudaStream_t>(stream), split, combine,
+                           n_combine, ws, ws_bytes);
 }
 
 extern "C" sp_status sp_attention(const void* q, int64_t ldq, int64_t q_rows, const void* k_pool,

@@ -84,6 +84,13 @@ struct Params {
   int64_t ldo;
   int kv_heads, group, block_size;
   float scale_log2;
+  // split-KV prefill (few CTAs, long causal rows): work entry w covers key
+  // tiles [split[w].x, split[w].y); split[w].z >= 0 -> unnormalised partial
+  // (O, m, l) into slot split[w].z * kv_heads + kvh, merged by
+  // prefill_combine_kernel.  NULL -> every entry covers all its key tiles.
+  const int4* split;
+  float* ws_o;   // [slots][256 rows][HD]
+  float* ws_ml;  // [slots][256 rows][2]
 };
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
@@ -160,7 +167,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int toks_per_tile = QROWS / G;
   const int tok_last = min(tok0 + 2 * toks_per_tile, q_len) - 1;
   const int kv_end = min(kv_len, fpos + tok_last + 1);
-  const int n_kt = (kv_end + KT - 1) / KT;
+  int j_begin = 0, n_kt = (kv_end + KT - 1) / KT, slot = -1;
+  if (p.split != nullptr) {
+    const int4 sp = p.split[blockIdx.x];
+    j_begin = sp.x;
+    n_kt = min(n_kt, sp.y);
+    slot = sp.z < 0 ? -1 : sp.z * p.kv_heads + kvh;
+  }
+  const int n_it = max(n_kt - j_begin, 0);  // iterations of this CTA (key tiles j_begin..n_kt-1)
   const int n_pages = (kv_len + p.block_size - 1) / p.block_size;
 
   if (warp == 8 && lane == 0) {
@@ -196,8 +210,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tma_load_3d(sQ + t * Q_TILE_BYTES + c * (Q_TILE_BYTES / 2), &tmQ, q_full, c * 64,
                       kvh * G, q_row0 + tok0 + t * toks_per_tile);
       const int32_t* bt = p.block_tables + (int64_t)item * p.bt_stride;
-      for (int j = 0; j < n_kt; ++j) {
-        const int s = j & 1;
+      for (int it = 0; it < n_it; ++it) {
+        const int j = j_begin + it, s = it & 1;
         uint8_t* sK = sKV + s * 2 * KV_TILE_BYTES;
         uint8_t* sV = sK + KV_TILE_BYTES;
         int rows[2];
@@ -210,12 +224,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // K and V slots are released separately: K(j) frees once both tiles'
         // QK(j) are done (an iteration before V(j) frees), so K(j+2) is in
         // flight a full iteration before QK(j+2) needs it
-        mbar_wait(k_empty + s, ((j >> 1) & 1) ^ 1);
+        mbar_wait(k_empty + s, ((it >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(k_full + s, KV_TILE_BYTES);
         for (int c = 0; c < 2; ++c)
           for (int h = 0; h < 2; ++h)
             tma_load_2d(sK + c * (KV_TILE_BYTES / 2) + h * 8192, &tmK, k_full + s, c * 64, rows[h]);
-        mbar_wait(v_empty + s, ((j >> 1) & 1) ^ 1);
+        mbar_wait(v_empty + s, ((it >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(v_full + s, KV_TILE_BYTES);
         for (int c = 0; c < 2; ++c)
           for (int h = 0; h < 2; ++h)
@@ -230,8 +244,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       constexpr uint32_t idesc_pv = idesc_bf16_f32(128, HD) | (1u << 16);  // B (V) MN-major
       const uint32_t sq = smem_u32(sQ);
       mbar_wait(q_full, 0);
-      auto issue_qk = [&](int t, int j) {
-        const int s = j & 1;
+      auto issue_qk = [&](int t, int it) {  // S_t of this CTA's it-th key tile
+        const int s = it & 1;
         const uint32_t sk = smem_u32(sKV + s * 2 * KV_TILE_BYTES);
         const uint32_t qa = sq + t * Q_TILE_BYTES;
         const uint32_t d_tmem = tmem + t * 128;
@@ -248,25 +262,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       issue_qk(0, 0);
       issue_qk(1, 0);
       umma_commit(k_empty + 0);
-      for (int j = 0; j < n_kt; ++j) {
-        const int s = j & 1;
-        const uint32_t par = (j >> 1) & 1;
+      for (int it = 0; it < n_it; ++it) {
+        const int s = it & 1;
+        const uint32_t par = (it >> 1) & 1;
         mbar_wait(v_full + s, par);
         const uint32_t sv = smem_u32(sKV + s * 2 * KV_TILE_BYTES + KV_TILE_BYTES);
-        const bool more = j + 1 < n_kt;
-        if (more) mbar_wait(k_full + (s ^ 1), ((j + 1) >> 1) & 1);
+        const bool more = it + 1 < n_it;
+        if (more) mbar_wait(k_full + (s ^ 1), ((it + 1) >> 1) & 1);
         for (int t = 0; t < 2; ++t) {
-          mbar_wait(p_full + t, j & 1);
+          mbar_wait(p_full + t, it & 1);
           tc_fence_after();
           const uint32_t p_tmem = tmem + t * 128;
           const uint32_t o_tmem = tmem + 256 + t * 128;
 #pragma unroll
           for (int k = 0; k < KT / 16; ++k) {
             umma_ts_bf16(o_tmem, p_tmem + k * 8, sdesc_sw128_mn(sv + k * 2048, KV_TILE_BYTES / 2),
-                         idesc_pv, (j | k) != 0 ? 1u : 0u);
+                         idesc_pv, (it | k) != 0 ? 1u : 0u);
           }
           if (more)
-            issue_qk(t, j + 1);
+            issue_qk(t, it + 1);
           else
             umma_commit(o_full + t);
         }
@@ -290,8 +304,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t s_tmem = tmem + lane_base + t * 128;
     const uint32_t o_tmem = tmem + lane_base + 256 + t * 128;
     float m_run = -INFINITY, l_run = 0.f;
-    for (int j = 0; j < n_kt; ++j) {
-      mbar_wait(s_full + t, j & 1);
+    for (int it = 0; it < n_it; ++it) {
+      const int j = j_begin + it;
+      mbar_wait(s_full + t, it & 1);
       tc_fence_after();
       float s[KT];  // raw scores; the softmax scale is folded into one FFMA below
 #pragma unroll
@@ -319,7 +334,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         m_run = m_new;
       }
       l_run *= corr;
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
+      if (it > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll 1
         for (int c = 0; c < HD / 32; ++c) {
           uint32_t r[32];
@@ -377,6 +392,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------- epilogue
     mbar_wait(o_full + t, 0);
     tc_fence_after();
+    if (slot >= 0) {  // split-KV: unnormalised partial O and (m, l), merged later
+      float* po = p.ws_o + ((int64_t)slot * 2 * QROWS + prow) * HD;
+#pragma unroll 1
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(o_tmem + c * 32, r);
+        tmem_ld_wait();
+        float4* d4 = reinterpret_cast<float4*>(po + c * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          d4[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                              __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+      }
+      float* pml = p.ws_ml + ((int64_t)slot * 2 * QROWS + prow) * 2;
+      pml[0] = m_run;
+      pml[1] = l_run;
+    } else {
     const float inv = 1.f / l_run;
     const bool store = tok < q_len;
     __nv_bfloat16* dst = p.out + (int64_t)(q_row0 + tok) * p.ldo + (int64_t)head * HD;
@@ -398,12 +430,67 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
+    }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 9) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
+  }
+}
+
+// Merge the split-KV partials of one (work tile, kv head): block = 32 packed
+// rows x 128 d (thread: one row, 16 d); entries of `combine` are (item, t0,
+// first split, n splits).  Splits are merged in ascending key order.
+__global__ void prefill_combine_kernel(const int4* __restrict__ combine, const Params p) {
+  pdl_wait();
+  pdl_trigger();
+  const int4 cb = combine[blockIdx.x];
+  const int kvh = blockIdx.y;
+  const int prow = blockIdx.z * 32 + (threadIdx.x >> 3);
+  const int c0 = (threadIdx.x & 7) * 16;
+  const int G = p.group;
+  const int q_row0 = p.cu_q[cb.x];
+  const int q_len = p.cu_q[cb.x + 1] - q_row0;
+  const int t = prow / QROWS;
+  const int tok = cb.y + t * (QROWS / G) + (prow % QROWS) / G;
+  if (tok >= q_len) return;
+  const int head = kvh * G + (prow % QROWS) % G;
+  float mx = -INFINITY;
+  for (int k = 0; k < cb.w; ++k) {
+    const int64_t slot = (int64_t)(cb.z + k) * p.kv_heads + kvh;
+    mx = fmaxf(mx, p.ws_ml[(slot * 2 * QROWS + prow) * 2]);
+  }
+  float l = 0.f, acc[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+  for (int k = 0; k < cb.w; ++k) {
+    const int64_t slot = (int64_t)(cb.z + k) * p.kv_heads + kvh;
+    const float* ml = p.ws_ml + (slot * 2 * QROWS + prow) * 2;
+    if (ml[0] == -INFINITY) continue;
+    const float f = exp2f(ml[0] - mx);
+    l += ml[1] * f;
+    const float4* o4 = reinterpret_cast<const float4*>(p.ws_o + (slot * 2 * QROWS + prow) * HD + c0);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float4 v = o4[e];
+      acc[4 * e] += v.x * f;
+      acc[4 * e + 1] += v.y * f;
+      acc[4 * e + 2] += v.z * f;
+      acc[4 * e + 3] += v.w * f;
+    }
+  }
+  const float inv = 1.f / l;
+  uint4* dst = reinterpret_cast<uint4*>(p.out + (int64_t)(q_row0 + tok) * p.ldo + (int64_t)head * HD + c0);
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    uint4 u;
+    u.x = pack_bf16x2(acc[8 * e] * inv, acc[8 * e + 1] * inv);
+    u.y = pack_bf16x2(acc[8 * e + 2] * inv, acc[8 * e + 3] * inv);
+    u.z = pack_bf16x2(acc[8 * e + 4] * inv, acc[8 * e + 5] * inv);
+    u.w = pack_bf16x2(acc[8 * e + 6] * inv, acc[8 * e + 7] * inv);
+    dst[e] = u;
   }
 }
 
@@ -414,7 +501,9 @@ int launch_prefill_tc(const void* q, int64_t ldq, int64_t q_rows_total, const vo
                       const void* v_pool, int64_t pool_rows, const int32_t* block_tables,
                       int64_t bt_stride, const int32_t* cu_q, const int32_t* first_pos,
                       const int32_t* kv_len, const int32_t* work, int n_work, void* out,
-                      int64_t ldo, int q_heads, int kv_heads, int block_size, cudaStream_t st);
+                      int64_t ldo, int q_heads, int kv_heads, int block_size, cudaStream_t st,
+                      const int32_t* split, const int32_t* combine, int n_combine, void* ws,
+                      int64_t ws_bytes);
 
 // tensor maps (shared cache with the GEMM)
 int tma_map_bf16(CUtensorMap* out, const void* ptr, int rank, const uint64_t* dims,
@@ -424,7 +513,9 @@ int launch_prefill_tc(const void* q, int64_t ldq, int64_t q_rows_total, const vo
                       const void* v_pool, int64_t pool_rows, const int32_t* block_tables,
                       int64_t bt_stride, const int32_t* cu_q, const int32_t* first_pos,
                       const int32_t* kv_len, const int32_t* work, int n_work, void* out,
-                      int64_t ldo, int q_heads, int kv_heads, int block_size, cudaStream_t st) {
+                      int64_t ldo, int q_heads, int kv_heads, int block_size, cudaStream_t st,
+                      const int32_t* split, const int32_t* combine, int n_combine, void* ws,
+                      int64_t ws_bytes) {
   using namespace attn_tc;
   const int G = q_heads / kv_heads;
   CUtensorMap tq, tk, tv;
@@ -456,13 +547,29 @@ int launch_prefill_tc(const void* q, int64_t ldq, int64_t q_rows_total, const vo
   p.group = G;
   p.block_size = block_size;
   p.scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
+  p.split = reinterpret_cast<const int4*>(split);
+  p.ws_o = p.ws_ml = nullptr;
+  if (split != nullptr) {
+    if (!ws) return fail(kInvalid, "attention split: workspace required");
+    p.ws_o = static_cast<float*>(ws);
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr = true;
   }
+  if (split != nullptr) {  // ws = [slots][256][HD] O partials, then [slots][256][2] (m, l)
+    const int64_t slots = ws_bytes / ((int64_t)2 * QROWS * (HD + 2) * 4);
+    p.ws_ml = p.ws_o + slots * 2 * QROWS * HD;
+  }
   launch_k(prefill_tc_kernel, dim3(n_work, kv_heads), NUM_THREADS, SMEM_BYTES, st, tq, tk, tv, p);
-  return check_launch("attn_prefill_tc_kernel");
+  if (int rc = check_launch("attn_prefill_tc_kernel")) return rc;
+  if (split != nullptr && n_combine > 0) {
+    launch_k(prefill_combine_kernel, dim3(n_combine, kv_heads, 2 * QROWS / 32), 256, 0, st,
+             reinterpret_cast<const int4*>(combine), p);
+    return check_launch("attn_prefill_combine_kernel");
+  }
+  return kOk;
 }
 
 }  // namespace sp

@@ -268,6 +268,7 @@ class Engine:
         self._pin_idx = 0
         # attention split-KV workspace, allocated once (graph replays need static buffers)
         self._ws = torch.empty(16 << 20, dtype=torch.float32, device=self.device)
+        self._sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         self.cuda_graphs = cuda_graphs
         self._fuse_splitk = os.environ.get("SP_FUSE_SPLITK", "1") != "0"
         self._graphs: Dict[tuple, _GraphEntry] = {}
@@ -466,6 +467,8 @@ class Engine:
             bt[i, :len(tab)] = tab
         ends = (cu[1:] - 1).astype(np.int32)
         decode_like = all(m == 1 for m in spans)
+        split = combine = None
+        n_slots = 0
         if decode_like:
             work = np.zeros((0, 2), dtype=np.int32)
         else:
@@ -473,6 +476,9 @@ class Engine:
             wl = [(i, t0, hist[i] + t0) for i in range(n) for t0 in range(0, spans[i], tt)]
             wl.sort(key=lambda w: -w[2])  # heaviest causal tiles first
             work = np.asarray([(i, t0) for i, t0, _ in wl], dtype=np.int32).reshape(-1, 2)
+            plan = self._split_plan(wl, spans, hist, tt)
+            if plan is not None:
+                work, split, combine, n_slots = plan
         # SP token shards: P of them, or s under SP(s) x TP(P/s)
         n_shards = self.sp_degree if mode is ParallelMode.SP else P
         bounds = shard_bounds(M, n_shards)
@@ -489,6 +495,9 @@ class Engine:
         parts = dict(toks=toks, pos=pos, slots=slots, cu=cu, first=first, kvlen=kvlen,
                      bt=bt.reshape(-1), ends=ends, work=work.reshape(-1),
                      tail_pos=tail_pos, tail_slot=tail_slot, tail_cu=tail_cu)
+        if split is not None:
+            parts["work_split"] = split.reshape(-1)
+            parts["work_combine"] = combine.reshape(-1)
         for r in range(n_shards):
             parts[f"sprows{r}"] = sp_rows[r]
         # every array starts on a 16-byte boundary (the kernels read int2 pairs)
@@ -519,6 +528,8 @@ class Engine:
         meta.bt = meta.bt.view(n, width)
         meta.work_pairs = meta.work
         meta.n_work = work.shape[0]
+        meta.n_combine = None if split is None else combine.shape[0]
+        meta.n_slots = n_slots
         meta.M, meta.n, meta.spans, meta.hist = M, n, spans, hist
         meta.ends_host = ends
         meta.bounds = bounds
@@ -531,6 +542,49 @@ class Engine:
         self.last_slots = slots
         self.last_block_table = bt
         return meta
+
+    def _split_plan(self, wl, spans, hist, tt):
+        """Split-KV plan for the tcgen05 prefill when the pass has too few
+        work tiles to fill the SMs (one long request under SP=8: 128 tiles x 1
+        kv head, causal costs 1..64 key tiles -> the longest tile alone set
+        the kernel time).  Tiles longer than a chunk are cut into key ranges
+        merged by the combine kernel; ~2 waves of balanced entries.  Returns
+        (work, split, combine, n_slots) or None (SP_ATTN_SPLIT=0 disables)."""
+        cfg = self.config
+        P = self.world_size
+        hk = cfg.kv_heads // P
+        if (os.environ.get("SP_ATTN_SPLIT") == "0" or cfg.head_dim != 128
+                or self.pool.block_size % 64 or len(wl) * hk >= self._sms):
+            return None
+        kt = 128  # key tile of the tcgen05 kernel
+        tiles = []
+        for i, t0, _ in wl:
+            q_end = min(t0 + tt, spans[i])
+            tiles.append((i, t0, -(-(hist[i] + q_end) // kt)))
+        total = sum(c for _, _, c in tiles)
+        # one wave: pieces of at most total/SMs key tiles, longest first (the
+        # block scheduler then packs them LPT-style); measured better than two
+        # waves of smaller pieces (per-CTA prologue, Q reload, partial traffic)
+        target = max(1, self._sms // hk)
+        chunk = max(2, -(-total // target))
+        entries, combine, slot = [], [], 0
+        for i, t0, c in tiles:
+            ns = -(-c // chunk)
+            if ns <= 1:
+                entries.append((c, i, t0, 0, c, -1))
+                continue
+            bounds = [c * k // ns for k in range(ns + 1)]
+            for k in range(ns):
+                entries.append((bounds[k + 1] - bounds[k], i, t0, bounds[k], bounds[k + 1], slot + k))
+            combine.append((i, t0, slot, ns))
+            slot += ns
+        if slot * hk * ops.SPLIT_SLOT_BYTES > self._ws.numel() * self._ws.element_size():
+            return None
+        entries.sort(key=lambda e: -e[0])
+        work = np.asarray([(e[1], e[2]) for e in entries], dtype=np.int32).reshape(-1, 2)
+        split = np.asarray([(e[3], e[4], e[5], 0) for e in entries], dtype=np.int32).reshape(-1, 4)
+        comb = np.asarray(combine, dtype=np.int32).reshape(-1, 4)
+        return work, split, comb, slot
 
     def _workspace(self, n_items: int, q_heads: int, max_kv: int) -> Optional[torch.Tensor]:
         # fixed 64 MB: the kernel falls back to one split when a pass would need more
@@ -555,13 +609,22 @@ class Engine:
         hist = [w - m for m, w in zip(spans, meta.windows)]
         causal = sum(m * t0 + m * (m + 1) // 2 for m, t0 in zip(spans, hist))
         kv_bytes = sum(meta.windows) * hk * d * 2 * 2
-        ops.attention(q, self.pool.layer_k(r, layer), self.pool.layer_v(r, layer), meta.bt, cu,
-                      first, meta.kvlen, out, n_items=meta.n,
-                      work=None if decode_like else meta.work_pairs,
-                      n_work=0 if decode_like else meta.n_work, max_q_len=max(spans),
-                      max_kv_len=meta.max_kv, q_heads=hq, kv_heads=hk, head_dim=d,
-                      block_size=self.pool.block_size, ws=ws, work_flops=4 * d * hq * causal,
-                      work_bytes=kv_bytes)
+        if not tails and not decode_like and meta.n_combine is not None:
+            ops.attention_prefill_split(
+                q, self.pool.layer_k(r, layer), self.pool.layer_v(r, layer), meta.bt, cu, first,
+                meta.kvlen, out, work=meta.work_pairs, split=meta.work_split,
+                n_work=meta.n_work, combine=meta.work_combine, n_combine=meta.n_combine,
+                n_slots=meta.n_slots, q_heads=hq, kv_heads=hk, head_dim=d,
+                block_size=self.pool.block_size, ws=self._ws, work_flops=4 * d * hq * causal,
+                work_bytes=kv_bytes)
+        else:
+            ops.attention(q, self.pool.layer_k(r, layer), self.pool.layer_v(r, layer), meta.bt,
+                          cu, first, meta.kvlen, out, n_items=meta.n,
+                          work=None if decode_like else meta.work_pairs,
+                          n_work=0 if decode_like else meta.n_work, max_q_len=max(spans),
+                          max_kv_len=meta.max_kv, q_heads=hq, kv_heads=hk, head_dim=d,
+                          block_size=self.pool.block_size, ws=ws,
+                          work_flops=4 * d * hq * causal, work_bytes=kv_bytes)
         # reference meter: per item per owned head, q·Kᵀ and P·V over the full window
         for m, w in zip(spans, meta.windows):
             meter.add_matmul(hq * m, d, w)

@@ -309,6 +309,31 @@ def attention(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
     _count(1 if n_work > 0 else 2)
 
 
+SPLIT_SLOT_BYTES = 256 * 130 * 4  # one (work entry, kv head) partial: O [256][128] + (m, l)
+
+
+def attention_prefill_split(q, k_pool, v_pool, block_tables, cu_q, first_pos, kv_len, out, *,
+                            work, split, n_work, combine, n_combine, n_slots, q_heads, kv_heads,
+                            head_dim, block_size, ws, work_flops: int = 0,
+                            work_bytes: int = 0) -> None:
+    """Split-KV tcgen05 prefill (sp_attention_prefill_split); ws must hold
+    n_slots * kv_heads partial slots."""
+    _need(q, torch.bfloat16, "attention q")
+    _need(out, torch.bfloat16, "attention out")
+    need = n_slots * kv_heads * SPLIT_SLOT_BYTES
+    if ws is None or ws.numel() * ws.element_size() < need:
+        raise ContractViolation("attention split: workspace too small")
+    with _Timed("attn_prefill", work_flops, work_bytes):
+        rc = _lib.load().sp_attention_prefill_split(
+            q.data_ptr(), q.stride(0), q.shape[0], k_pool.data_ptr(), v_pool.data_ptr(),
+            k_pool.shape[0], block_tables.data_ptr(), block_tables.stride(0), cu_q.data_ptr(),
+            first_pos.data_ptr(), kv_len.data_ptr(), work.data_ptr(), split.data_ptr(), n_work,
+            _ptr(combine), n_combine, out.data_ptr(), out.stride(0), q_heads, kv_heads, head_dim,
+            block_size, ws.data_ptr(), need, _stream())
+    _lib.check(rc, "sp_attention_prefill_split")
+    _count(2 if n_combine else 1)
+
+
 def a2a_pack(src: torch.Tensor, dst: torch.Tensor, rows: int, peers: int, width: int) -> None:
     if rows == 0:
         return

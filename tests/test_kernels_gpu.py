@@ -517,3 +517,57 @@ def test_rmsnorm_block_size_invariant(h):
     ops.add_rmsnorm(small_x, gain, 1e-5, small, add=add[:, :few].contiguous(), n_add=2)  # wide
     assert torch.equal(small_x, big_x[:few])
     assert torch.equal(small, big[:few])
+
+
+@pytest.mark.parametrize("chunk", [1, 2, 3])
+def test_attention_prefill_split_kv(chunk):
+    """Split-KV tcgen05 prefill: each work tile's key tiles cut into ranges of
+    `chunk`, partials merged by the combine kernel; equals the reference (and
+    the unsplit kernel) within bf16 tolerance, deterministic run to run."""
+    d, hq, hk, bs = 128, 8, 2, 64
+    spans, hist = [300, 129, 1], [0, 200, 700]
+    ks, vs, qs = [], [], []
+    for m, t0 in zip(spans, hist):
+        ks.append(rnd(t0 + m, hk, d, seed=120 + m))
+        vs.append(rnd(t0 + m, hk, d, seed=140 + m))
+        qs.append(rnd(m, hq, d, seed=160 + m))
+    kpool, bt = _paged(ks, hk, d, bs)
+    vpool = torch.zeros_like(kpool)
+    for i, t in enumerate(vs):
+        tab = bt[i].tolist()
+        for j in range(t.shape[0]):
+            vpool[tab[j // bs], :, j % bs] = t[j]
+    q = torch.cat(qs).view(-1, hq * d)
+    M = q.shape[0]
+    cu = torch.tensor([0] + list(np.cumsum(spans)), dtype=torch.int32, device="cuda")
+    first = torch.tensor(hist, dtype=torch.int32, device="cuda")
+    kvl = torch.tensor([a + b for a, b in zip(spans, hist)], dtype=torch.int32, device="cuda")
+    tt = ops.attn_tile_tokens(hq, hk, d, bs)
+    work, split, combine, slot = [], [], [], 0
+    for i, m in enumerate(spans):
+        for t0 in range(0, m, tt):
+            n_kt = -(-(hist[i] + min(t0 + tt, m)) // 128)
+            ns = -(-n_kt // chunk)
+            if ns == 1:
+                work.append((i, t0)); split.append((0, n_kt, -1, 0))
+                continue
+            for k in range(ns):
+                work.append((i, t0)); split.append((k * chunk, min(n_kt, (k + 1) * chunk), slot + k, 0))
+            combine.append((i, t0, slot, ns))
+            slot += ns
+    T = lambda a: torch.tensor(a, dtype=torch.int32, device="cuda").view(-1)
+    ws = torch.empty(max(1, slot) * hk * ops.SPLIT_SLOT_BYTES // 4, device="cuda")
+    outs = []
+    for _ in range(2):
+        out = torch.empty(M, hq * d, device="cuda", dtype=torch.bfloat16)
+        ops.attention_prefill_split(q, kpool, vpool, bt, cu, first, kvl, out, work=T(work),
+                                    split=T(split), n_work=len(work), combine=T(combine),
+                                    n_combine=len(combine), n_slots=max(1, slot), q_heads=hq,
+                                    kv_heads=hk, head_dim=d, block_size=bs, ws=ws)
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
+    lo = 0
+    for i, (m, t0) in enumerate(zip(spans, hist)):
+        want = _attn_ref(qs[i], ks[i], vs[i], t0)
+        assert rel(outs[0][lo:lo + m].view(m, hq, d), want) < 2e-2, i
+        lo += m
