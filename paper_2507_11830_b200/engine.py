@@ -578,8 +578,8 @@ class Engine:
                 entries.append((bounds[k + 1] - bounds[k], i, t0, bounds[k], bounds[k + 1], slot + k))
             combine.append((i, t0, slot, ns))
             slot += ns
-        if slot * hk * ops.SPLIT_SLOT_BYTES > self._ws.numel() * self._ws.element_size():
-            return None
+        if slot == 0 or slot * hk * ops.SPLIT_SLOT_BYTES > self._ws.numel() * self._ws.element_size():
+            return None  # nothing long enough to split, or no workspace for it
         entries.sort(key=lambda e: -e[0])
         work = np.asarray([(e[1], e[2]) for e in entries], dtype=np.int32).reshape(-1, 2)
         split = np.asarray([(e[3], e[4], e[5], 0) for e in entries], dtype=np.int32).reshape(-1, 4)
