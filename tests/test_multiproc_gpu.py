@@ -63,6 +63,8 @@ def _tiny(world):
     from oracle.model import init_weights_llama, llama_tiny_config
     if world == 4:  # P | kv_heads
         return init_weights_llama(llama_tiny_config(max_seq=512, n_kv_heads=4), seed=1)
+    if world == 8:
+        return init_weights_llama(llama_tiny_config(max_seq=512, n_kv_heads=8), seed=2)
     return init_weights_llama(llama_tiny_config(max_seq=512), seed=0)
 
 
@@ -92,7 +94,8 @@ def _worker(rank, world, port, q, sp_degree=None):
 
 
 @pytest.mark.parametrize("world,sp_degree,fused", [(2, None, False), (4, 2, False),
-                                                   (2, None, True), (4, None, True)])
+                                                   (2, None, True), (4, None, True),
+                                                   (8, None, True), (8, 4, True)])
 def test_multi_process_engine_matches_loopback(world, sp_degree, fused, monkeypatch):
     """(2, None): pure SP/TP over two processes, bit-identical; (4, 2): the
     SP(2) x TP(2) base config over four processes (TP-group all-reduces on
@@ -115,7 +118,7 @@ def test_multi_process_engine_matches_loopback(world, sp_degree, fused, monkeypa
              for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=300) for _ in procs)
+    res = dict(q.get(timeout=600) for _ in procs)
     for p in procs:
         p.join(timeout=120)
     for r in range(world):
