@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* p_full = bars + 9;   // [2] per Q tile
   uint64_t* o_full = bars + 11;  // [2] per Q tile
   uint64_t* v_empty = bars + 13; // [2] V slot free (both tiles' PV done)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  uint64_t* p_half = bars + 15;  // [2] per Q tile: P of keys 0-63 stored (PV may start)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int2 wk = p.work[blockIdx.x];
@@ -188,7 +189,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(k_empty + s, 1);
       mbar_init(v_empty + s, 1);
       mbar_init(s_full + s, 1);
-      mbar_init(p_full + s, 128);
+      mbar_init(p_full + s, 4);  // one arrival per softmax warp
+      mbar_init(p_half + s, 4);
       mbar_init(o_full + s, 1);
     }
     fence_barrier_init();
@@ -270,14 +272,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool more = it + 1 < n_it;
         if (more) mbar_wait(k_full + (s ^ 1), ((it + 1) >> 1) & 1);
         for (int t = 0; t < 2; ++t) {
-          mbar_wait(p_full + t, it & 1);
-          tc_fence_after();
           const uint32_t p_tmem = tmem + t * 128;
           const uint32_t o_tmem = tmem + 256 + t * 128;
+          // P·V in two halves: keys 0-63 start while the softmax finishes 64-127
 #pragma unroll
-          for (int k = 0; k < KT / 16; ++k) {
-            umma_ts_bf16(o_tmem, p_tmem + k * 8, sdesc_sw128_mn(sv + k * 2048, KV_TILE_BYTES / 2),
-                         idesc_pv, (it | k) != 0 ? 1u : 0u);
+          for (int h = 0; h < 2; ++h) {
+            mbar_wait((h == 0 ? p_half : p_full) + t, it & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int k = h * (KT / 32); k < (h + 1) * (KT / 32); ++k) {
+              umma_ts_bf16(o_tmem, p_tmem + k * 8, sdesc_sw128_mn(sv + k * 2048, KV_TILE_BYTES / 2),
+                           idesc_pv, (it | k) != 0 ? 1u : 0u);
+            }
           }
           if (more)
             issue_qk(t, it + 1);
@@ -381,13 +387,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           pk[e] = pack_bf16x2(a, b);
         }
         tmem_st32(s_tmem + c * 32, pk);
+        if (c == 0) {  // first half of P ready: let P·V start on keys 0-63
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(p_half + t);
+        }
       }
       float sa, sb;
       f2_unpack(sum2, sa, sb);
       l_run += sa + sb;
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(p_full + t);
+      __syncwarp();  // every lane's P stores complete before the warp's single arrival
+      if (lane == 0) mbar_arrive(p_full + t);
     }
     // ------------------------------------------------------------- epilogue
     mbar_wait(o_full + t, 0);
