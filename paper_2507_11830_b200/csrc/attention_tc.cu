@@ -30,15 +30,17 @@ namespace attn_tc {
 constexpr int HD = 128;
 constexpr int QROWS = 128;       // rows per Q tile
 constexpr int KT = 128;          // keys per tile
-// Softmax exponential variants (tools/kbench.py attn, 8K causal, after the K/V
-// release split): 4 of every 32 pairs through the FMA-pipe polynomial
-// (ATTN_POLY_PAIRS=4) measured best, 1190 vs 1140 TFLOP/s all-MUFU (8: 1178,
-// 16: 1114); one MUFU.EX2.bf16x2 per pair (ATTN_EXP_BF16X2=1) was slower (1077).
+// Softmax exponential variants (tools/kbench.py attn, 8K causal): with the K/V
+// release split alone, 4 of every 32 pairs through the FMA-pipe polynomial
+// (ATTN_POLY_PAIRS=4) was best (1190 vs 1140 TFLOP/s all-MUFU); once P·V
+// starts per half of P the SFU is off the critical path and all-MUFU is as
+// fast or faster (1210 vs 1195), so the default is 0.  One MUFU.EX2.bf16x2
+// per pair (ATTN_EXP_BF16X2=1) was slower (1077).
 #ifndef ATTN_EXP_BF16X2
 #define ATTN_EXP_BF16X2 0
 #endif
 #ifndef ATTN_POLY_PAIRS
-#define ATTN_POLY_PAIRS 4
+#define ATTN_POLY_PAIRS 0
 #endif
 constexpr int kPolyPairs = ATTN_POLY_PAIRS;  // of 32 pairs per 64 columns (tools/kbench.py attn)
 
