@@ -519,19 +519,18 @@ __global__ void __launch_bounds__(NUM_THREADS, SwapTile<NT>::CTAS_PER_SM)
         const int ks = it % p.ksplit, t = it / p.ksplit;
         const int kb0 = ks * p.kb_per_split, kb1 = min(p.k_blocks, kb0 + p.kb_per_split);
         const int row0 = t * WT * 128;
-        const int wv = min(WT, (p.N - row0 + 127) / 128);  // weight tiles inside N
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           uint8_t* sw = smem + stage * STAGE_BYTES;
-          mbar_arrive_expect_tx(full + stage, wv * W_TILE + T::X_BYTES);
+          // one 256-row box = both 128-row weight tiles (rows past N zero-filled)
+          mbar_arrive_expect_tx(full + stage, WT * W_TILE + T::X_BYTES);
           const int k = kb * BK;
           int ko = 0, kc = k;
           if (p.a_kchunk > 0) {
             ko = k / p.a_kchunk;
             kc = k - ko * p.a_kchunk;
           }
-          for (int w = 0; w < wv; ++w)  // weights: no dependency on the predecessor
-            tma_load_2d(sw + w * W_TILE, &tmW, full + stage, k, row0 + w * 128);
+          tma_load_2d(sw, &tmW, full + stage, k, row0);  // weights: no dependency on the predecessor
           if (waited) {
             tma_load_3d(sw + T::W_BYTES, &tmX, full + stage, kc, 0, ko);
           } else {
@@ -1173,7 +1172,7 @@ static int launch_swap(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   {
     uint64_t dims[2] = {(uint64_t)K, (uint64_t)N};
     uint64_t strides[1] = {(uint64_t)ldb * 2};
-    uint32_t box[2] = {BK, 128};
+    uint32_t box[2] = {BK, (uint32_t)(swp::WT * 128)};
     if (int rc = get_map(&tw, B, 2, dims, strides, box)) return rc;
   }
   Params p;
