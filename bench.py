@@ -62,6 +62,16 @@ def peaks():
     return p
 
 
+def workload_config(args, world: int) -> dict:
+    """The workload both arms report (BASELINE configs[1]); how the reference
+    arm samples it is stated in its cpu_baseline.sample."""
+    name = "llama-3.1-8b-geometry single-request 8K-token prefill, Ulysses SP"
+    if args.layers:
+        name += f" (TRUNCATED to {args.layers} layers: debug only, not a bench value)"
+    return {"workload": name, "seq_len": args.seq, "requests": 1, "parallelism": f"sp{world}",
+            "l2": "inputs larger than L2 (16 GB of weights streamed per step)"}
+
+
 def traffic_per_launch(kernel: str):
     """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
     capture of this workload (profiles/r01_traffic.json, tools/ncu_traffic.py)."""
@@ -179,14 +189,11 @@ def run_reference(args):
             vals.append(v)
     v = statistics.mean(vals)
     cb = smp.describe(v)
-    threads = smp.p
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 8192 / v * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "llama-3.1-8b single-request 8K prefill (per-layer sample)",
-                       "model": "llama-3.1-8b", "seq_len": args.seq, "global_batch": 1,
-                       "parallelism": f"sp{threads} (host threads)"},
+            "config": workload_config(args, args.gpus),
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -408,10 +415,7 @@ def run_ours(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (random-init N(0,0.02^2) bf16 weights, uniform token ids)",
-                "config": {"workload": "llama-3.1-8b single-request 8K-token prefill, Ulysses SP",
-                           "model": "llama-3.1-8b" + ("" if not args.layers else f"-L{args.layers}-INVALID"),
-                           "seq_len": args.seq, "global_batch": 1, "parallelism": f"sp{world}",
-                           "l2": "inputs larger than L2 (16 GB of weights streamed per step)"},
+                "config": workload_config(args, world),
                 "roofline": roofline, "attention": attn, "whole_step": whole,
                 "decode": decode, "decode_tpot_ms": decode["tpot_ms"] if decode else None,
                 "e2e": {"value": round(e2e_val, 1), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
