@@ -207,6 +207,49 @@ class _GraphEntry:
         self.failed = False  # capture raised: this key stays eager
 
 
+def attention_split_plan(wl, spans, hist, tt: int, hk: int, sms: int, max_slots: int):
+    """Split-KV plan for a prefill pass whose work tiles x kv heads do not
+    fill the SMs (one long request under SP=8: 128 tiles x 1 kv head with
+    causal costs 1..64 key tiles, so the longest tile alone set the kernel
+    time).  Tiles longer than total/(SMs/kv heads) key tiles are cut into
+    nearly equal key ranges, merged later by the combine kernel; entries are
+    ordered longest first so the block scheduler packs them into ~one wave.
+
+    wl: (item, t0, key0) work tiles; returns (work [n,2], split [n,4] =
+    (first key tile, end key tile, slot | -1, 0), combine [c,4] = (item, t0,
+    first slot, n slots), n_slots) or None when nothing needs splitting."""
+    if len(wl) * hk >= sms:
+        return None
+    kt = 128  # key tile of the tcgen05 kernel
+    tiles = []
+    for i, t0, _ in wl:
+        q_end = min(t0 + tt, spans[i])
+        tiles.append((i, t0, -(-(hist[i] + q_end) // kt)))
+    total = sum(c for _, _, c in tiles)
+    # one wave: pieces of at most total/SMs key tiles, longest first (the
+    # block scheduler then packs them LPT-style); measured better than two
+    # waves of smaller pieces (per-CTA prologue, Q reload, partial traffic)
+    chunk = max(2, -(-total // max(1, sms // hk)))
+    entries, combine, slot = [], [], 0
+    for i, t0, c in tiles:
+        ns = -(-c // chunk)
+        if ns <= 1:
+            entries.append((c, i, t0, 0, c, -1))
+            continue
+        bounds = [c * k // ns for k in range(ns + 1)]
+        for k in range(ns):
+            entries.append((bounds[k + 1] - bounds[k], i, t0, bounds[k], bounds[k + 1], slot + k))
+        combine.append((i, t0, slot, ns))
+        slot += ns
+    if slot == 0 or slot > max_slots:
+        return None  # nothing long enough to split, or no workspace for it
+    entries.sort(key=lambda e: -e[0])
+    work = np.asarray([(e[1], e[2]) for e in entries], dtype=np.int32).reshape(-1, 2)
+    split = np.asarray([(e[3], e[4], e[5], 0) for e in entries], dtype=np.int32).reshape(-1, 4)
+    comb = np.asarray(combine, dtype=np.int32).reshape(-1, 4)
+    return work, split, comb, slot
+
+
 class Engine:
     def __init__(self, weights: ModelWeights, group: DeviceGroup, policy: ShiftPolicy,
                  swiftkv: Optional[SwiftKvConfig] = None, *, num_blocks: Optional[int] = None,
@@ -544,47 +587,15 @@ class Engine:
         return meta
 
     def _split_plan(self, wl, spans, hist, tt):
-        """Split-KV plan for the tcgen05 prefill when the pass has too few
-        work tiles to fill the SMs (one long request under SP=8: 128 tiles x 1
-        kv head, causal costs 1..64 key tiles -> the longest tile alone set
-        the kernel time).  Tiles longer than a chunk are cut into key ranges
-        merged by the combine kernel; ~2 waves of balanced entries.  Returns
-        (work, split, combine, n_slots) or None (SP_ATTN_SPLIT=0 disables)."""
+        """Split-KV plan for the tcgen05 prefill (see attention_split_plan);
+        None when not needed, not applicable or disabled (SP_ATTN_SPLIT=0)."""
         cfg = self.config
-        P = self.world_size
-        hk = cfg.kv_heads // P
+        hk = cfg.kv_heads // self.world_size
         if (os.environ.get("SP_ATTN_SPLIT") == "0" or cfg.head_dim != 128
-                or self.pool.block_size % 64 or len(wl) * hk >= self._sms):
+                or self.pool.block_size % 64):
             return None
-        kt = 128  # key tile of the tcgen05 kernel
-        tiles = []
-        for i, t0, _ in wl:
-            q_end = min(t0 + tt, spans[i])
-            tiles.append((i, t0, -(-(hist[i] + q_end) // kt)))
-        total = sum(c for _, _, c in tiles)
-        # one wave: pieces of at most total/SMs key tiles, longest first (the
-        # block scheduler then packs them LPT-style); measured better than two
-        # waves of smaller pieces (per-CTA prologue, Q reload, partial traffic)
-        target = max(1, self._sms // hk)
-        chunk = max(2, -(-total // target))
-        entries, combine, slot = [], [], 0
-        for i, t0, c in tiles:
-            ns = -(-c // chunk)
-            if ns <= 1:
-                entries.append((c, i, t0, 0, c, -1))
-                continue
-            bounds = [c * k // ns for k in range(ns + 1)]
-            for k in range(ns):
-                entries.append((bounds[k + 1] - bounds[k], i, t0, bounds[k], bounds[k + 1], slot + k))
-            combine.append((i, t0, slot, ns))
-            slot += ns
-        if slot == 0 or slot * hk * ops.SPLIT_SLOT_BYTES > self._ws.numel() * self._ws.element_size():
-            return None  # nothing long enough to split, or no workspace for it
-        entries.sort(key=lambda e: -e[0])
-        work = np.asarray([(e[1], e[2]) for e in entries], dtype=np.int32).reshape(-1, 2)
-        split = np.asarray([(e[3], e[4], e[5], 0) for e in entries], dtype=np.int32).reshape(-1, 4)
-        comb = np.asarray(combine, dtype=np.int32).reshape(-1, 4)
-        return work, split, comb, slot
+        max_slots = self._ws.numel() * self._ws.element_size() // (hk * ops.SPLIT_SLOT_BYTES)
+        return attention_split_plan(wl, spans, hist, tt, hk, self._sms, max_slots)
 
     def _workspace(self, n_items: int, q_heads: int, max_kv: int) -> Optional[torch.Tensor]:
         # fixed 64 MB: the kernel falls back to one split when a pass would need more

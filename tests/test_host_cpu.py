@@ -222,3 +222,40 @@ def test_presets_validate():
     with pytest.raises(ConfigError):
         tiny_llama().check_world(4)  # 2 kv heads cannot split 4 ways
     assert llama31_8b().hidden == 4096 and llama33_70b().n_layers == 80
+
+
+def test_attention_split_plan_covers_every_key_tile_once():
+    """Split-KV plan (SP=8 shape: one 8K request, 4 q / 1 kv head per rank):
+    every work tile's key tiles are covered exactly once by its entries, split
+    tiles own contiguous slots listed in their combine entry, no piece exceeds
+    the chunk, entries are longest first; enough tiles -> no plan."""
+    from paper_2507_11830_b200.engine import attention_split_plan
+    T, tt = 8192, 64
+    wl = sorted([(0, t0, t0) for t0 in range(0, T, tt)], key=lambda w: -w[2])
+    plan = attention_split_plan(wl, [T], [0], tt, hk=1, sms=148, max_slots=4096)
+    assert plan is not None
+    work, split, comb, n_slots = plan
+    sizes = split[:, 1] - split[:, 0]
+    assert (sizes > 0).all() and list(sizes) == sorted(sizes, reverse=True)
+    total = sum(-(-(t0 + tt) // 128) for _, t0, _ in wl)
+    assert sizes.max() <= max(2, -(-total // 148))
+    cover = {}
+    for (i, t0), (jb, je, slot, _) in zip(work.tolist(), split.tolist()):
+        cover.setdefault((i, t0), []).append((jb, je, slot))
+    slots_seen = []
+    for (i, t0), parts in cover.items():
+        parts.sort()
+        n_kt = -(-(t0 + tt) // 128)
+        assert parts[0][0] == 0 and parts[-1][1] == n_kt
+        assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+        if len(parts) == 1:
+            assert parts[0][2] == -1
+        else:
+            c = [x for x in comb.tolist() if (x[0], x[1]) == (i, t0)]
+            assert len(c) == 1 and c[0][3] == len(parts)
+            assert [p[2] for p in parts] == list(range(c[0][2], c[0][2] + len(parts)))
+            slots_seen += [p[2] for p in parts]
+    assert sorted(slots_seen) == list(range(n_slots))
+    # a pass that already fills the GPU, or a workspace too small: no plan
+    assert attention_split_plan(wl, [T], [0], tt, hk=8, sms=148, max_slots=4096) is None
+    assert attention_split_plan(wl, [T], [0], tt, hk=1, sms=148, max_slots=1) is None
