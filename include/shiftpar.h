@@ -207,12 +207,14 @@ sp_status sp_peer_scatter_rows(const void* src, int64_t lds, int rows_total, int
 sp_status sp_peer_signal(const unsigned long long* flag_ptrs, int peers, int my_rank, void* stream);
 sp_status sp_peer_wait(int* flags, int peers, void* stream);
 /* TP all-reduce fused into the residual add + RMSNorm (parallel_engine.py
- * :371-372, :379 + :354): x[r] += sum_s part_s[r] (ascending s, partials
- * [rows, hidden] f32 at part_ptrs[s]); if out != NULL also writes the bf16
- * RMSNorm of the updated row. */
-sp_status sp_peer_allreduce_add_rmsnorm(const unsigned long long* part_ptrs, int peers, float* x,
-                                        int64_t ldx, const float* gain, float eps, void* out_bf16,
-                                        int64_t ldo, int rows, int hidden, void* stream);
+ * :371-372, :379 + :354): x[r] += sum_s part_s[r] (ascending rank s; rank s's
+ * partial is its `slabs` K-split slabs [slabs][rows][hidden] f32 at
+ * part_ptrs[s], summed in ascending order first); if out != NULL also writes
+ * the bf16 RMSNorm of the updated row. */
+sp_status sp_peer_allreduce_add_rmsnorm(const unsigned long long* part_ptrs, int peers, int slabs,
+                                        float* x, int64_t ldx, const float* gain, float eps,
+                                        void* out_bf16, int64_t ldo, int rows, int hidden,
+                                        void* stream);
 
 /* ---------------------------------------------- reductions and heads
  * In-process (loopback) all-reduce: dst = a + b, f32, ascending order as in

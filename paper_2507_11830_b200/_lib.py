@@ -34,7 +34,8 @@ SIGNATURES = {
     "sp_peer_scatter_rows": (_c_int, [_vp, _i64, _c_int, _c_int, _c_int, _c_int, _vp, _vp]),
     "sp_peer_signal": (_c_int, [_vp, _c_int, _c_int, _vp]),
     "sp_peer_wait": (_c_int, [_vp, _c_int, _vp]),
-    "sp_peer_allreduce_add_rmsnorm": (_c_int, [_vp, _c_int, _vp, _i64, _vp, _f32, _vp, _i64, _c_int,
+    "sp_peer_allreduce_add_rmsnorm": (_c_int, [_vp, _c_int, _c_int, _vp, _i64, _vp, _f32, _vp, _i64,
+                                               _c_int,
                                                _c_int, _vp]),
     "sp_embed": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _vp]),
     "sp_add_rmsnorm": (_c_int, [_vp, _i64, _vp, _c_int, _vp, _f32, _vp, _vp, _i64, _c_int, _c_int,

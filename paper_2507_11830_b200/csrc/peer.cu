@@ -75,7 +75,8 @@ __global__ void peer_wait_kernel(int* flags, int peers) {
 // and (if out != NULL) writes bf16( gain * x / sqrt(mean(x^2) + eps) ).
 template <int VEC>
 __global__ void peer_allreduce_norm_kernel(const unsigned long long* __restrict__ part_ptrs,
-                                           int peers, float* __restrict__ x, int64_t ldx,
+                                           int peers, int slabs, int64_t slab_stride,
+                                           float* __restrict__ x, int64_t ldx,
                                            const float* __restrict__ gain, float eps,
                                            __nv_bfloat16* __restrict__ out, int64_t ldo,
                                            int hidden) {
@@ -84,21 +85,33 @@ __global__ void peer_allreduce_norm_kernel(const unsigned long long* __restrict_
   const int r = blockIdx.x;
   float* xr = x + (int64_t)r * ldx;
   float v[VEC * 4];
-  float ss = 0.f;
+  float ssq[VEC];
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
     const int c = (i * blockDim.x + threadIdx.x) * 4;
     float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
     if (c < hidden) {
-      float4 sum = *reinterpret_cast<const float4*>(
-          reinterpret_cast<const float*>(part_ptrs[0]) + (int64_t)r * hidden + c);
-      for (int s = 1; s < peers; ++s) {
-        const float4 q = *reinterpret_cast<const float4*>(
-            reinterpret_cast<const float*>(part_ptrs[s]) + (int64_t)r * hidden + c);
-        sum.x += q.x;
-        sum.y += q.y;
-        sum.z += q.z;
-        sum.w += q.w;
+      // rank partial = its K-split slabs summed in ascending order (what the
+      // GEMM's own split-K reduce would have written); ranks in ascending order
+      float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s = 0; s < peers; ++s) {
+        const float* base = reinterpret_cast<const float*>(part_ptrs[s]) + (int64_t)r * hidden + c;
+        float4 q = *reinterpret_cast<const float4*>(base);
+        for (int k = 1; k < slabs; ++k) {
+          const float4 b = *reinterpret_cast<const float4*>(base + k * slab_stride);
+          q.x += b.x;
+          q.y += b.y;
+          q.z += b.z;
+          q.w += b.w;
+        }
+        if (s == 0) {
+          sum = q;
+        } else {
+          sum.x += q.x;
+          sum.y += q.y;
+          sum.z += q.z;
+          sum.w += q.w;
+        }
       }
       t = *reinterpret_cast<const float4*>(xr + c);
       t.x += sum.x;
@@ -111,22 +124,11 @@ __global__ void peer_allreduce_norm_kernel(const unsigned long long* __restrict_
     v[4 * i + 1] = t.y;
     v[4 * i + 2] = t.z;
     v[4 * i + 3] = t.w;
-    ss += t.x * t.x + t.y * t.y + t.z * t.z + t.w * t.w;
+    ssq[i] = ((t.x * t.x + t.y * t.y) + t.z * t.z) + t.w * t.w;
   }
   if (out == nullptr) return;
-  __shared__ float red[32];
-#pragma unroll
-  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float q = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-    if (threadIdx.x == 0) red[0] = q;
-  }
-  __syncthreads();
-  const float den = sqrtf(red[0] / (float)hidden + eps);
+  __shared__ float red[256];
+  const float den = sqrtf(rms_chunk_sum<VEC>(ssq, hidden, red) / (float)hidden + eps);
   __nv_bfloat16* orow = out + (int64_t)r * ldo;
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
@@ -146,22 +148,25 @@ __global__ void peer_allreduce_norm_kernel(const unsigned long long* __restrict_
 using namespace sp;
 
 extern "C" sp_status sp_peer_allreduce_add_rmsnorm(const unsigned long long* part_ptrs, int peers,
-                                                   float* x, int64_t ldx, const float* gain,
-                                                   float eps, void* out_bf16, int64_t ldo,
-                                                   int rows, int hidden, void* stream) {
-  if (!part_ptrs || peers < 1 || rows < 0 || hidden <= 0 || hidden % 4 || ldx % 4 || ldo % 4)
+                                                   int slabs, float* x, int64_t ldx,
+                                                   const float* gain, float eps, void* out_bf16,
+                                                   int64_t ldo, int rows, int hidden,
+                                                   void* stream) {
+  if (!part_ptrs || peers < 1 || slabs < 1 || rows < 0 || hidden <= 0 || hidden % 4 || ldx % 4 ||
+      ldo % 4)
     return fail(kInvalid, "peer_allreduce_add_rmsnorm: bad arguments");
   if (out_bf16 && !gain) return fail(kInvalid, "peer_allreduce_add_rmsnorm: gain needed with out");
   if (rows == 0) return kOk;
-  const int threads = 256;
+  const int64_t slab_stride = (int64_t)rows * hidden;
+  const int threads = norm_block_threads(rows, hidden);
   const int per = (hidden + threads * 4 - 1) / (threads * 4);
   auto out = static_cast<__nv_bfloat16*>(out_bf16);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   switch (per) {
-    case 1: launch_k(peer_allreduce_norm_kernel<1>, rows, threads, 0, st, part_ptrs, peers, x, ldx, gain, eps, out, ldo, hidden); break;
-    case 2: launch_k(peer_allreduce_norm_kernel<2>, rows, threads, 0, st, part_ptrs, peers, x, ldx, gain, eps, out, ldo, hidden); break;
-    case 3: case 4: launch_k(peer_allreduce_norm_kernel<4>, rows, threads, 0, st, part_ptrs, peers, x, ldx, gain, eps, out, ldo, hidden); break;
-    case 5: case 6: case 7: case 8: launch_k(peer_allreduce_norm_kernel<8>, rows, threads, 0, st, part_ptrs, peers, x, ldx, gain, eps, out, ldo, hidden); break;
+    case 1: launch_k(peer_allreduce_norm_kernel<1>, rows, threads, 0, st, part_ptrs, peers, slabs, slab_stride, x, ldx, gain, eps, out, ldo, hidden); break;
+    case 2: launch_k(peer_allreduce_norm_kernel<2>, rows, threads, 0, st, part_ptrs, peers, slabs, slab_stride, x, ldx, gain, eps, out, ldo, hidden); break;
+    case 3: case 4: launch_k(peer_allreduce_norm_kernel<4>, rows, threads, 0, st, part_ptrs, peers, slabs, slab_stride, x, ldx, gain, eps, out, ldo, hidden); break;
+    case 5: case 6: case 7: case 8: launch_k(peer_allreduce_norm_kernel<8>, rows, threads, 0, st, part_ptrs, peers, slabs, slab_stride, x, ldx, gain, eps, out, ldo, hidden); break;
     default: return fail(kUnsupported, "peer_allreduce_add_rmsnorm: hidden > 8192");
   }
   return check_launch("peer_allreduce_norm_kernel");

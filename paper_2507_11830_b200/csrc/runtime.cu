@@ -116,32 +116,9 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, int64_t ldx, const flo
     v[4 * i + 3] = t.w;
     ssq[i] = ((t.x * t.x + t.y * t.y) + t.z * t.z) + t.w * t.w;
   }
-  // Sum of squares in an order defined on float4 CHUNKS, not threads (chunk q
-  // = i * blockDim + tid): butterfly inside each group of 32 consecutive
-  // chunks, then the group sums in ascending stride-32 order and a final
-  // butterfly — identical bits for any block size, so the launcher may pick
-  // the block size by row count.
   __shared__ float red[256];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_groups = (hidden / 4 + 31) / 32;
-#pragma unroll
-  for (int i = 0; i < VEC; ++i) {
-    float s = ssq[i];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const int grp = i * (blockDim.x >> 5) + warp;
-    if (lane == 0 && grp < n_groups) red[grp] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float s = 0.f;
-    for (int g = lane; g < n_groups; g += 32) s += red[g];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) red[0] = s;
-  }
-  __syncthreads();
-  const float den = sqrtf(red[0] / (float)hidden + eps);
+  const float ss = rms_chunk_sum<VEC>(ssq, hidden, red);
+  const float den = sqrtf(ss / (float)hidden + eps);
   __nv_bfloat16* orow = out + (int64_t)r * ldo;
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
@@ -401,13 +378,7 @@ extern "C" sp_status sp_add_rmsnorm(float* x, int64_t ldx, const float* add, int
     return fail(kInvalid, "add_rmsnorm: hidden and strides must be multiples of 4");
   if (rows == 0) return kOk;
   if (add && row_idx) return fail(kInvalid, "add_rmsnorm: add with row_idx unsupported");
-  // Few rows (a decode pass: one CTA per row) -> one float4 per thread, up to
-  // 1024 threads, so each row's loads are spread wide; many rows (prefill) ->
-  // 256-thread blocks (measured: 1024 costs ~2.5% of an 8K prefill, 256 costs
-  // ~5% of a B=64 decode).  The kernel's reduction order does not depend on
-  // the block size, so results are bit-identical either way.
-  const int wide = std::min(1024, std::max(32, ((hidden / 4 + 31) / 32) * 32));
-  int threads = rows <= 2 * 148 ? wide : std::min(wide, std::max(256, ((hidden / 32 + 31) / 32) * 32));
+  int threads = norm_block_threads(rows, hidden);
   if (const char* e = getenv("SP_NORM_THREADS")) threads = atoi(e);
   const int per = (hidden + threads * 4 - 1) / (threads * 4);
   auto out = static_cast<__nv_bfloat16*>(out_bf16);

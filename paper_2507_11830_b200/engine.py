@@ -699,11 +699,13 @@ class Engine:
         # fused one-shot all-reduce over peer memory (partials -> peers' sum in the norm kernel)
         peer = self._peer if (self._peer is not None and M <= self._peer.max_tokens) else None
         peer_pending = False
+        peer_slabs = [1, 1]   # K-split slabs per rank in the peer partial buffers (O, down)
         split_pending = None  # (K-split partials of the last projection, count) -> next norm
         for layer in range(n_full):
             lw = w.layers[layer]
             if peer_pending:
-                ops.peer_allreduce_add_rmsnorm(peer.part_ptrs[1], P, x, lw.attn_gain, eps, xn, M)
+                ops.peer_allreduce_add_rmsnorm(peer.part_ptrs[1], P, x, lw.attn_gain, eps, xn, M,
+                                               slabs=peer_slabs[1])
             elif split_pending is not None:
                 ops.add_rmsnorm(x, lw.attn_gain, eps, xn, add=split_pending[0],
                                 n_add=split_pending[1])
@@ -732,17 +734,16 @@ class Engine:
                     split_pending = self._proj_residual(o, wo, x, M, h, hqw, cfg.n_heads * d,
                                                         meters[r], fuse=True)
                 else:
-                    part = (peer.part[r][0][:M] if peer is not None
-                            else torch.empty((M, h), dtype=torch.float32, device=dev))
-                    ops.gemm(o, wo, part, ops.EPI_STORE_F32, M=M, N=h, K=hqw, lda=hqw,
-                             ldb=cfg.n_heads * d, ldd=h, meter=meters[r])
+                    part, peer_slabs[0] = self._tp_partial(peer, r, 0, o, wo, M, hqw,
+                                                           cfg.n_heads * d, meters[r])
                     parts[r] = part
                     if peer is not None:
                         ops.peer_signal(peer.tp_flag_ptrs[0], P, r)
             xn2 = torch.empty((M, h), dtype=torch.bfloat16, device=dev)
             if peer is not None:
                 self._peer_reduce_wait(0, parts)
-                ops.peer_allreduce_add_rmsnorm(peer.part_ptrs[0], P, x, lw.mlp_gain, eps, xn2, M)
+                ops.peer_allreduce_add_rmsnorm(peer.part_ptrs[0], P, x, lw.mlp_gain, eps, xn2, M,
+                                               slabs=peer_slabs[0])
             elif split_pending is not None:
                 ops.add_rmsnorm(x, lw.mlp_gain, eps, xn2, add=split_pending[0],
                                 n_add=split_pending[1])
@@ -760,10 +761,8 @@ class Engine:
                     split_pending = self._proj_residual(act, wd, x, M, h, fl, cfg.ffn_dim,
                                                         meters[r], fuse=layer < n_full - 1)
                 else:
-                    part = (peer.part[r][1][:M] if peer is not None
-                            else torch.empty((M, h), dtype=torch.float32, device=dev))
-                    ops.gemm(act, wd, part, ops.EPI_STORE_F32, M=M, N=h, K=fl, lda=fl,
-                             ldb=cfg.ffn_dim, ldd=h, meter=meters[r])
+                    part, peer_slabs[1] = self._tp_partial(peer, r, 1, act, wd, M, fl,
+                                                           cfg.ffn_dim, meters[r])
                     parts[r] = part
                     if peer is not None:
                         ops.peer_signal(peer.tp_flag_ptrs[1], P, r)
@@ -773,7 +772,8 @@ class Engine:
             else:
                 pending = g.all_reduce_sum(parts)[g.local_ranks[0]] if P > 1 else None
         if peer_pending:
-            ops.peer_allreduce_add_rmsnorm(peer.part_ptrs[1], P, x, None, eps, None, M)
+            ops.peer_allreduce_add_rmsnorm(peer.part_ptrs[1], P, x, None, eps, None, M,
+                                           slabs=peer_slabs[1])
         elif pending is not None:
             ops.add_f32(x, pending, x)
         if cut is not None:
@@ -796,6 +796,28 @@ class Engine:
             parts[r] = lg
         logits = self._gather_vocab(parts, n_rows)
         return self._split(logits, meta, span_logits and cut is None)
+
+    def _tp_partial(self, peer, r, which, a, w, M, K, ldb, meter):
+        """Rank r's TP partial of a residual projection (O: which=0, down: 1).
+        With peer buffers in the split-K (decode) regime the GEMM leaves its
+        K-split slabs there and the one-shot all-reduce kernel sums them (no
+        reduce kernel); returns (partial tensor, slabs per rank)."""
+        h = self.config.hidden
+        if peer is None:
+            part = torch.empty((M, h), dtype=torch.float32, device=self.device)
+            ops.gemm(a, w, part, ops.EPI_STORE_F32, M=M, N=h, K=K, lda=K, ldb=ldb, ldd=h,
+                     meter=meter)
+            return part, 1
+        n = self._partials(M, h, K)
+        if n > 1 and n * M <= peer.max_tokens:
+            slabs = peer.part[r][which].view(-1)[:n * M * h].view(n, M, h)
+            ops.gemm(a, w, slabs, ops.EPI_PARTIAL_F32, M=M, N=h, K=K, lda=K, ldb=ldb, ldd=h,
+                     meter=meter)
+            return slabs[0], n
+        part = peer.part[r][which][:M]
+        ops.gemm(a, w, part, ops.EPI_STORE_F32, M=M, N=h, K=K, lda=K, ldb=ldb, ldd=h,
+                 meter=meter)
+        return part, 1
 
     def _peer_reduce_wait(self, which: int, parts: Dict[int, torch.Tensor]) -> None:
         """Ledger + completion wait of a fused TP all-reduce (flag rows 2/3)."""

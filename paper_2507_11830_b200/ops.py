@@ -173,13 +173,15 @@ def peer_wait(flags: torch.Tensor, peers: int) -> None:
 
 def peer_allreduce_add_rmsnorm(part_ptrs: torch.Tensor, peers: int, x: torch.Tensor,
                                gain: Optional[torch.Tensor], eps: float,
-                               out: Optional[torch.Tensor], rows: int) -> None:
-    """x += sum of the P peer partials (ascending rank), then optional RMSNorm."""
+                               out: Optional[torch.Tensor], rows: int, slabs: int = 1) -> None:
+    """x += sum of the P peer partials (ascending rank; each rank's partial is
+    its `slabs` K-split slabs [slabs][rows][h] summed first), then optional
+    RMSNorm."""
     if rows == 0:
         return
     _lib.check(_lib.load().sp_peer_allreduce_add_rmsnorm(
-        part_ptrs.data_ptr(), peers, x.data_ptr(), x.stride(0), _ptr(gain), float(eps), _ptr(out),
-        0 if out is None else out.stride(0), rows, x.shape[1], _stream()),
+        part_ptrs.data_ptr(), peers, slabs, x.data_ptr(), x.stride(0), _ptr(gain), float(eps),
+        _ptr(out), 0 if out is None else out.stride(0), rows, x.shape[1], _stream()),
         "sp_peer_allreduce_add_rmsnorm")
     _count()
 

@@ -464,6 +464,40 @@ def test_gemm_partials_fused_into_rmsnorm_bitexact(M, N, K):
         ops.set_gemm_workspace(None)
 
 
+@pytest.mark.parametrize("P,M,N,K", [(2, 16, 4096, 4096), (4, 3, 4096, 3584), (2, 200, 1024, 2048)])
+def test_peer_allreduce_from_partial_slabs_bitexact(P, M, N, K):
+    """The one-shot TP all-reduce reading each rank's K-split slabs (the O/down
+    GEMM's EPI_PARTIAL_F32 output, no reduce kernel) equals the all-reduce of
+    the GEMM-reduced partials (EPI_STORE_F32), x and the normed output alike."""
+    ops.set_gemm_workspace(torch.empty(64 << 20, dtype=torch.uint8, device="cuda"))
+    try:
+        n = ops.gemm_partials(M, N, K)
+        x0 = torch.randn(M, N, device="cuda")
+        gain = torch.rand(N, device="cuda") + 0.5
+        slabs, whole = [], []
+        for r in range(P):
+            a, b = rnd(M, K, seed=70 + r), rnd(N, K, seed=80 + r)
+            s = torch.full((n, M, N), float("nan"), device="cuda")
+            ops.gemm(a, b, s, ops.EPI_PARTIAL_F32, M=M, N=N, K=K, lda=K, ldb=K, ldd=N)
+            w = torch.empty(M, N, device="cuda")
+            ops.gemm(a, b, w, ops.EPI_STORE_F32, M=M, N=N, K=K, lda=K, ldb=K, ldd=N)
+            slabs.append(s)
+            whole.append(w)
+        outs = []
+        for bufs, k in ((slabs, n), (whole, 1)):
+            ptrs = torch.tensor([t.data_ptr() for t in bufs], dtype=torch.int64, device="cuda")
+            x = x0.clone()
+            o = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+            ops.peer_allreduce_add_rmsnorm(ptrs, P, x, gain, 1e-5, o, M, slabs=k)
+            outs.append((x, o))
+        assert torch.equal(outs[0][0], outs[1][0])
+        assert torch.equal(outs[0][1], outs[1][1])
+        want = x0 + sum(w for w in whole)
+        assert rel(outs[0][0], want) < 1e-5
+    finally:
+        ops.set_gemm_workspace(None)
+
+
 def test_rope_kv_write_from_partials_bitexact():
     """QKV projection left as K-split partials, reduced inside RoPE + KV write,
     equals the bf16 projection (reduced by the GEMM) fed to RoPE + KV write."""
