@@ -161,6 +161,7 @@ class CpuSample:
         eng.step([(s, toks)], mode="sp")
         dt = time.perf_counter() - t0
         eng.group.close()
+        self.last_ms = dt * 1e3
         return self.tokens / dt / self.layers_model
 
     def describe(self, value: float) -> dict:
@@ -182,16 +183,20 @@ def run_reference(args):
     if rank != 0:
         return
     smp = CpuSample(host_threads())
-    vals = []
+    vals, ms = [], []
     for i in range(args.warmup + args.steps):
         v = smp.run()
         if i >= args.warmup:
             vals.append(v)
+            ms.append(smp.last_ms)
     v = statistics.mean(vals)
     cb = smp.describe(v)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 8192 / v * 1e3, "higher_is_better": True, "scaling": "strong",
+            # a step is the bounded sample (wall clock); the full 8K prefill it stands for
+            # would take ms_per_full_step_extrapolated
+            "ms_per_step": statistics.mean(ms), "ms_per_full_step_extrapolated": 8192 / v * 1e3,
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(args, args.gpus),
             "cpu_baseline": cb,

@@ -71,8 +71,17 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, int64_t ldx, const flo
                                    float eps,
                                    const int32_t* __restrict__ row_idx,
                                    __nv_bfloat16* __restrict__ out, int64_t ldo, int hidden) {
+  // the gain is a weight (never written by a predecessor): fetched before the wait
+  float4 g[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = (i * blockDim.x + threadIdx.x) * 4;
+    g[i] = out && c < hidden ? *reinterpret_cast<const float4*>(gain + c)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   pdl_wait();  // inputs of this kernel are written by its predecessor
   pdl_trigger();
+  constexpr int BATCH = VEC == 1 ? 12 : 4;  // partial loads in flight together
   const int r = blockIdx.x;
   const int64_t src_row = row_idx ? row_idx[r] : r;
   float* xr = x + src_row * ldx;
@@ -87,14 +96,14 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, int64_t ldx, const flo
       t = *reinterpret_cast<const float4*>(xr + c);
       if (ar) {
         float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int s0 = 0; s0 < n_add; s0 += 4) {  // ascending: the split-K / all-reduce order
-          float4 b[4];
+        for (int s0 = 0; s0 < n_add; s0 += BATCH) {  // ascending: the split-K / all-reduce order
+          float4 b[BATCH];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)  // loads of a batch in flight together
+          for (int u = 0; u < BATCH; ++u)
             b[u] = s0 + u < n_add ? *reinterpret_cast<const float4*>(ar + (s0 + u) * add_stride + c)
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < BATCH; ++u) {
             if (s0 + u < n_add) {
               a.x += b[u].x;
               a.y += b[u].y;
@@ -124,10 +133,9 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, int64_t ldx, const flo
   for (int i = 0; i < VEC; ++i) {
     const int c = (i * blockDim.x + threadIdx.x) * 4;
     if (c < hidden) {
-      float4 g = *reinterpret_cast<const float4*>(gain + c);
       uint2 u;
-      u.x = pack_bf16x2(g.x * (v[4 * i + 0] / den), g.y * (v[4 * i + 1] / den));
-      u.y = pack_bf16x2(g.z * (v[4 * i + 2] / den), g.w * (v[4 * i + 3] / den));
+      u.x = pack_bf16x2(g[i].x * (v[4 * i + 0] / den), g[i].y * (v[4 * i + 1] / den));
+      u.y = pack_bf16x2(g[i].z * (v[4 * i + 2] / den), g[i].w * (v[4 * i + 3] / den));
       *reinterpret_cast<uint2*>(orow + c) = u;
     }
   }
