@@ -28,5 +28,6 @@ from .fabric import DeviceGroup, LoopbackGroup, NcclGroup  # noqa: F401
 from .flops import FlopMeter, PassShape, flop_count, shard_bounds, shard_rows  # noqa: F401
 from .kv_cache import AXIS_ORDER, BlockAllocator, KvCache, KvPool, LayoutFingerprint  # noqa: F401
 from .weights import ModelWeights  # noqa: F401
+from . import spec_decode  # noqa: F401,E402
 
 __version__ = "0.1.0"
