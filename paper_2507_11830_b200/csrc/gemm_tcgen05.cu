@@ -421,7 +421,10 @@ struct SwapTile {
   static constexpr int RING = (CTAS_PER_SM == 2 ? 108 : 200) * 1024;
   static constexpr int STAGES = RING / STAGE_BYTES > 10 ? 10 : RING / STAGE_BYTES;
   static constexpr int ACC_COLS = swp::WT * NT;  // one accumulator stage
-  static constexpr int TMEM_COLS = 2 * ACC_COLS < 32 ? 32 : 2 * ACC_COLS;
+  // NT = 256 (M in (128, 256]): both 128-row halves x 256 tokens fill all 512
+  // TMEM columns, so a single accumulator stage (one item per CTA anyway)
+  static constexpr int ACC_STAGES = NT >= 256 ? 1 : 2;
+  static constexpr int TMEM_COLS = ACC_STAGES * ACC_COLS < 32 ? 32 : ACC_STAGES * ACC_COLS;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
@@ -478,6 +481,7 @@ __global__ void __launch_bounds__(NUM_THREADS, SwapTile<NT>::CTAS_PER_SM)
   using T = SwapTile<NT>;
   using namespace swp;
   constexpr int STAGES = T::STAGES, STAGE_BYTES = T::STAGE_BYTES, TMEM_COLS = T::TMEM_COLS;
+  constexpr int ACC_STAGES = T::ACC_STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -1131,7 +1135,7 @@ static int64_t swap_splits(int N, int K, int sms) {
 // the swap-AB (decode) regime applies: one 128-row M tile that cannot cover the SMs
 static bool swap_regime(int M, int N, int sms) {
   using namespace sp::gemm;
-  return cdiv(M, BM) == 1 && cdiv(N, 256) < sms && N % 32 == 0 &&
+  return M <= 256 && cdiv(N, 256) < sms && N % 32 == 0 &&
          getenv("SP_GEMM_NO_SPLITK") == nullptr;
 }
 
@@ -1288,7 +1292,8 @@ extern "C" int sp_gemm_partials(int M, int N, int K) {
   if (!swap_regime(M, N, sms)) return 1;
   if (M <= 32) return (int)swap_splits<32>(N, K, sms);
   if (M <= 64) return (int)swap_splits<64>(N, K, sms);
-  return (int)swap_splits<128>(N, K, sms);
+  if (M <= 128) return (int)swap_splits<128>(N, K, sms);
+  return (int)swap_splits<256>(N, K, sms);
 }
 
 extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
@@ -1315,38 +1320,39 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
   if (reinterpret_cast<uintptr_t>(D) & 15) return fail(kInvalid, "gemm: D must be 16-byte aligned");
 
   // Regime selection (numerics are identical within a regime):
-  //  * enough 128x256 tiles to cover the SMs        -> BN=256
-  //  * one M tile (decode-size M)                   -> swap-AB over 256-row weight
-  //    super tiles, K split just enough to cover ~2/3 of the SMs in one round;
-  //    split partials summed in ascending split order by splitk_reduce_kernel
+  //  * decode-size M (<= 256) with fewer 256-row weight super tiles than SMs
+  //                                                  -> swap-AB weight streaming over
+  //    256-row super tiles (tokens padded to NT = 32/64/128/256), K split just
+  //    enough to cover the SMs in one round; split partials summed in ascending
+  //    split order (splitk_reduce_kernel, or the consumer for EPI_PARTIAL_F32)
+  //  * enough 128x256 tiles to cover the SMs        -> BN=256 (2-CTA pairs)
   //  * otherwise                                     -> narrower N tiles (128/64/32),
   //    bit-identical to BN=256 (same K loop)
   const int sms = sm_count();
   const int64_t m_tiles = cdiv(M, BM);
-  const int64_t k_blocks = cdiv(K, BK);
   int bn = 256;
-  if (m_tiles * cdiv(N, 256) < sms) {
-    if (swap_regime(M, N, sms)) {
-      // decode-size M: swap-AB weight streaming (+ split-K / fused epilogue)
-      int rc = -1;
-      if (M <= 32)
-        rc = launch_swap<32>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
-                             peer_width, peer_stride, stream, g_ws, g_ws_bytes);
-      else if (M <= 64)
-        rc = launch_swap<64>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
-                             peer_width, peer_stride, stream, g_ws, g_ws_bytes);
-      else
-        rc = launch_swap<128>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
-                              peer_width, peer_stride, stream, g_ws, g_ws_bytes);
-      if (rc >= 0) return rc;
-    }
-    if (epilogue != SP_EPI_SWIGLU) {
-      bn = 32;
-      for (int c : {128, 64}) {
-        if (m_tiles * cdiv(N, c) >= sms) {
-          bn = c;
-          break;
-        }
+  if (swap_regime(M, N, sms)) {
+    int rc = -1;
+    if (M <= 32)
+      rc = launch_swap<32>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
+                           peer_width, peer_stride, stream, g_ws, g_ws_bytes);
+    else if (M <= 64)
+      rc = launch_swap<64>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
+                           peer_width, peer_stride, stream, g_ws, g_ws_bytes);
+    else if (M <= 128)
+      rc = launch_swap<128>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
+                            peer_width, peer_stride, stream, g_ws, g_ws_bytes);
+    else
+      rc = launch_swap<256>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
+                            peer_width, peer_stride, stream, g_ws, g_ws_bytes);
+    if (rc >= 0) return rc;
+  }
+  if (m_tiles * cdiv(N, 256) < sms && epilogue != SP_EPI_SWIGLU) {
+    bn = 32;
+    for (int c : {128, 64}) {
+      if (m_tiles * cdiv(N, c) >= sms) {
+        bn = c;
+        break;
       }
     }
   }

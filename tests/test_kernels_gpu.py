@@ -315,6 +315,7 @@ def test_gemm_tile_width_variants_are_bitexact(monkeypatch):
     """The N-tile variants (256/128/64/32, picked by M and N) share the K loop, so
     an output element does not depend on which variant computed it."""
     monkeypatch.setenv("SP_GEMM_NO_SPLITK", "1")
+    monkeypatch.setenv("SP_GEMM_NO_SPLITK", "1")  # M = 200 would take the swap-AB regime
     M, N, K = 200, 768, 1024
     a, b = rnd(M, K, seed=30), rnd(N, K, seed=31)
     outs = {}
@@ -332,7 +333,7 @@ def test_gemm_tile_width_variants_are_bitexact(monkeypatch):
 
 
 @pytest.mark.parametrize("N,K", [(1024, 4096), (2560, 512), (384, 192), (128256, 128)])
-@pytest.mark.parametrize("M", [1, 48, 100])
+@pytest.mark.parametrize("M", [1, 48, 100, 200, 256])
 @pytest.mark.parametrize("epi", ["f32", "add", "bf16", "swiglu", "gelu", "peer", "chunked"])
 def test_gemm_split_k_regime(epi, M, N, K):
     """Decode-size M: swap-AB stream-K (equal weight share per CTA; super tiles
