@@ -448,7 +448,11 @@ __device__ __forceinline__ uint32_t kv_addr(uint32_t base, int key, int c16) {
 
 __global__ void __launch_bounds__(NUM_THREADS, 2) decode_tma_kernel(
     const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Params p) {
-  pdl_wait();  // inputs of this kernel are written by its predecessor
+  // PDL: the block table, lengths and every KV page before the new token were
+  // written by earlier passes / host copies (complete once this grid can
+  // launch), so the producer streams the first ring of those pages BEFORE
+  // griddepcontrol.wait; only Q and the page holding the new token (written
+  // by the predecessor RoPE + KV-write kernel) wait for it.
   pdl_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -476,25 +480,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 2) decode_tma_kernel(
     }
     fence_barrier_init();
   }
-  if (warp < NCONS) {
-    constexpr int NCH = HD / 8;
-    for (int i = tid; i < 16 * NCH; i += NCONS * 32) {
-      const int r = i / NCH, c = i % NCH;
-      const bool ok = r < G;
-      const __nv_bfloat16* src = p.q;
-      if (ok) src = p.q + (int64_t)q_row * p.ldq + (int64_t)(kvh * G + r) * HD + c * 8;
-      cp_async16(sQ + r * HD + swz<HD>(r, c) * 8, src, ok);
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-  }
-  __syncthreads();
+  __syncthreads();  // barriers initialised
 
   float o[HD / 8][4];
   float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
   if (warp == NCONS) {
     if (lane == 0) {
+      const int old_tiles = (kv_len - 1) / PAGE;  // tiles whose keys all precede the new token
+      bool waited = false;
       for (int t = t_begin, i = 0; t < t_end; ++t, ++i) {
+        if (!waited && (i >= STAGES || t >= old_tiles)) {
+          pdl_wait();
+          waited = true;
+        }
         const int s = i % STAGES;
         mbar_wait(empty + s, ((i / STAGES) & 1) ^ 1);
         const int key0 = t * PAGE;
@@ -507,9 +505,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 2) decode_tma_kernel(
         tma_load_2d(st + TILE_BYTES, &tmV, full + s, 0, row);
         tma_load_2d(st + TILE_BYTES + TILE_BYTES / 2, &tmV, full + s, 64, row);
       }
+      if (!waited) pdl_wait();
     }
     __syncwarp();
   } else {
+    pdl_wait();  // Q is written by the predecessor
+    {
+      constexpr int NCH = HD / 8;
+      for (int i = tid; i < 16 * NCH; i += NCONS * 32) {
+        const int r = i / NCH, c = i % NCH;
+        const bool ok = r < G;
+        const __nv_bfloat16* src = p.q;
+        if (ok) src = p.q + (int64_t)q_row * p.ldq + (int64_t)(kvh * G + r) * HD + c * 8;
+        cp_async16(sQ + r * HD + swz<HD>(r, c) * 8, src, ok);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      asm volatile("bar.sync 1, %0;" ::"n"(NCONS * 32) : "memory");  // consumer warps only
+    }
     uint32_t qf[HD / 16][4];
     load_q_frags<HD>(qf, sQ, 0, lane);
 #pragma unroll

@@ -261,8 +261,11 @@ def test_attention_prefill_paged_causal(d, hq, hk, bs):
 
 
 @pytest.mark.parametrize("d,hq,hk,ctx", [(128, 32, 8, 2048), (128, 8, 2, 100), (64, 4, 4, 5000),
-                                         (32, 8, 2, 1)])
+                                         (32, 8, 2, 1), (128, 8, 2, 5000), (128, 32, 2, 700),
+                                         (128, 64, 8, 300)])
 def test_attention_decode_split_kv(d, hq, hk, ctx):
+    """Split-KV decode (TMA kernel with the first ring of old pages streamed
+    before the PDL wait; splits merged by the combine kernel) vs the reference."""
     n = 5
     bs = 64
     ctxs = [ctx + 7 * i for i in range(n)]
