@@ -2,8 +2,9 @@
 
 Every wrapper validates its operands, forwards raw device pointers and the
 current CUDA stream to libshiftpar.so, and maps a nonzero status to
-``ContractViolation``.  ``launch_count`` counts the kernels enqueued (the
-``gpu_launches`` figure of bench.py).
+``ContractViolation``.  ``kernel_launches()`` counts the kernels enqueued (the
+``gpu_launches`` figure of bench.py): the C-side launch counter plus the kernel
+nodes of replayed CUDA graphs.
 """
 
 from __future__ import annotations
@@ -23,17 +24,10 @@ EPI_SWIGLU = 3
 EPI_GELU = 4
 EPI_PARTIAL_F32 = 5  # raw K-split partials [n][M][N], n = gemm_partials(M, N, K)
 
-launch_count = 0
-
 # Optional live per-kernel timing (bench.py roofline): when set to a dict, the
 # wrapped launches record CUDA events on the launching stream plus their
 # algorithmic work: PROFILE[kind] -> list of (start, end, flops, bytes).
 PROFILE: Optional[dict] = None
-
-
-def _count(n: int = 1) -> None:
-    global launch_count
-    launch_count += n
 
 
 class _Timed:
@@ -115,7 +109,6 @@ def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, epilogue: int, *, M:
                               d.data_ptr(), ldd, M, N, K, epilogue, peer_width, peer_stride,
                               _stream())
     _lib.check(rc, "sp_gemm_bf16")
-    _count()
 
 
 _gemm_ws: Optional[torch.Tensor] = None
@@ -146,7 +139,6 @@ def gemm_to_peers(a: torch.Tensor, b: torch.Tensor, peer_ptrs: torch.Tensor, *, 
                                                b.data_ptr(), ldb, peer_ptrs.data_ptr(), row_off,
                                                ldd, M, N, K, epilogue, peer_width, _stream())
     _lib.check(rc, "sp_gemm_bf16_to_peers")
-    _count()
 
 
 def peer_scatter_rows(src: torch.Tensor, rows_total: int, peers: int, my_rank: int,
@@ -157,18 +149,15 @@ def peer_scatter_rows(src: torch.Tensor, rows_total: int, peers: int, my_rank: i
     _lib.check(_lib.load().sp_peer_scatter_rows(src.data_ptr(), src.stride(0), rows_total,
                                                 src.shape[1], peers, my_rank, dst_ptrs.data_ptr(),
                                                 _stream()), "sp_peer_scatter_rows")
-    _count()
 
 
 def peer_signal(flag_ptrs: torch.Tensor, peers: int, my_rank: int) -> None:
     _lib.check(_lib.load().sp_peer_signal(flag_ptrs.data_ptr(), peers, my_rank, _stream()),
                "sp_peer_signal")
-    _count()
 
 
 def peer_wait(flags: torch.Tensor, peers: int) -> None:
     _lib.check(_lib.load().sp_peer_wait(flags.data_ptr(), peers, _stream()), "sp_peer_wait")
-    _count()
 
 
 def peer_allreduce_add_rmsnorm(part_ptrs: torch.Tensor, peers: int, x: torch.Tensor,
@@ -183,7 +172,6 @@ def peer_allreduce_add_rmsnorm(part_ptrs: torch.Tensor, peers: int, x: torch.Ten
         part_ptrs.data_ptr(), peers, slabs, x.data_ptr(), x.stride(0), _ptr(gain), float(eps),
         _ptr(out), 0 if out is None else out.stride(0), rows, x.shape[1], _stream()),
         "sp_peer_allreduce_add_rmsnorm")
-    _count()
 
 
 def embed(ids: torch.Tensor, table: torch.Tensor, out: torch.Tensor,
@@ -197,7 +185,6 @@ def embed(ids: torch.Tensor, table: torch.Tensor, out: torch.Tensor,
     rc = _lib.load().sp_embed(ids.data_ptr(), table.data_ptr(), _ptr(pos), _ptr(pos_table),
                               out.data_ptr(), rows, table.shape[1], _stream())
     _lib.check(rc, "sp_embed")
-    _count()
 
 
 def ipc_export(t: torch.Tensor) -> tuple:
@@ -240,7 +227,6 @@ def add_rmsnorm(x: torch.Tensor, gain: torch.Tensor, eps: float, out: torch.Tens
                                     float(eps), _ptr(row_idx), out.data_ptr(), out.stride(0), n, h,
                                     _stream())
     _lib.check(rc, "sp_add_rmsnorm")
-    _count()
 
 
 def rope_kv_write(qkv: torch.Tensor, pos: torch.Tensor, slot: torch.Tensor,
@@ -256,7 +242,6 @@ def rope_kv_write(qkv: torch.Tensor, pos: torch.Tensor, slot: torch.Tensor,
                                       k_pool.data_ptr(), v_pool.data_ptr(), rows, q_heads,
                                       kv_heads, head_dim, block_size, _stream())
     _lib.check(rc, "sp_rope_kv_write")
-    _count()
 
 
 def rope_kv_write_partials(parts: torch.Tensor, n_parts: int, pos: torch.Tensor,
@@ -276,7 +261,6 @@ def rope_kv_write_partials(parts: torch.Tensor, n_parts: int, pos: torch.Tensor,
         _ptr(q_out), 0 if q_out is None else q_out.stride(0), k_pool.data_ptr(),
         v_pool.data_ptr(), rows, q_heads, kv_heads, head_dim, block_size, _stream())
     _lib.check(rc, "sp_rope_kv_write_partials")
-    _count()
 
 
 def attn_tile_tokens(q_heads: int, kv_heads: int, head_dim: int, block_size: int) -> int:
@@ -308,7 +292,6 @@ def attention(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
                                       out.data_ptr(), out.stride(0), q_heads, kv_heads, head_dim,
                                       block_size, _ptr(ws), ws_bytes, _stream())
     _lib.check(rc, "sp_attention")
-    _count(1 if n_work > 0 else 2)
 
 
 SPLIT_SLOT_BYTES = 256 * 130 * 4  # one (work entry, kv head) partial: O [256][128] + (m, l)
@@ -333,7 +316,6 @@ def attention_prefill_split(q, k_pool, v_pool, block_tables, cu_q, first_pos, kv
             _ptr(combine), n_combine, out.data_ptr(), out.stride(0), q_heads, kv_heads, head_dim,
             block_size, ws.data_ptr(), need, _stream())
     _lib.check(rc, "sp_attention_prefill_split")
-    _count(2 if n_combine else 1)
 
 
 def a2a_pack(src: torch.Tensor, dst: torch.Tensor, rows: int, peers: int, width: int) -> None:
@@ -341,7 +323,6 @@ def a2a_pack(src: torch.Tensor, dst: torch.Tensor, rows: int, peers: int, width:
         return
     _lib.check(_lib.load().sp_a2a_pack(src.data_ptr(), src.stride(0), dst.data_ptr(), rows, peers,
                                        width, _stream()), "sp_a2a_pack")
-    _count()
 
 
 def a2a_unpack(src: torch.Tensor, dst: torch.Tensor, rows: int, peers: int, width: int) -> None:
@@ -349,7 +330,6 @@ def a2a_unpack(src: torch.Tensor, dst: torch.Tensor, rows: int, peers: int, widt
         return
     _lib.check(_lib.load().sp_a2a_unpack(src.data_ptr(), dst.data_ptr(), dst.stride(0), rows,
                                          peers, width, _stream()), "sp_a2a_unpack")
-    _count()
 
 
 def add_f32(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor) -> None:
@@ -359,7 +339,6 @@ def add_f32(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor) -> None:
         return
     _lib.check(_lib.load().sp_add_f32(a.data_ptr(), b.data_ptr(), out.data_ptr(), n, _stream()),
                "sp_add_f32")
-    _count()
 
 
 def argmax(logits: torch.Tensor, idx: torch.Tensor, val: Optional[torch.Tensor] = None) -> None:
@@ -369,7 +348,6 @@ def argmax(logits: torch.Tensor, idx: torch.Tensor, val: Optional[torch.Tensor] 
         return
     _lib.check(_lib.load().sp_argmax(logits.data_ptr(), logits.stride(0), rows, vocab,
                                      idx.data_ptr(), _ptr(val), _stream()), "sp_argmax")
-    _count()
 
 
 def gather_rows(src: torch.Tensor, idx: torch.Tensor, dst: torch.Tensor) -> None:
@@ -379,4 +357,3 @@ def gather_rows(src: torch.Tensor, idx: torch.Tensor, dst: torch.Tensor) -> None
     _lib.check(_lib.load().sp_gather_rows_f32(src.data_ptr(), src.stride(0), idx.data_ptr(),
                                               dst.data_ptr(), dst.stride(0), rows, src.shape[1],
                                               _stream()), "sp_gather_rows_f32")
-    _count()
