@@ -234,16 +234,32 @@ def test_flops_and_comm_counts(c1):
 
 
 def test_sp_comm_bytes_follow_gqa_formula(c1):
-    """P·SP/TP bytes = L(2H+2Hkv)d / ((4L+... )h) with GQA."""
+    """check_comm_ratio (verify_checks.py:177-194) with GQA:
+    per device and pass, TP moves 2L f32 all-reduces of [M, h] (ring bytes
+    2(P-1)/P each; no embedding all-reduce), SP moves L fused q|k|v
+    all-to-alls + L back all-to-alls of bf16 rows ((P-1)/P of what a rank
+    sends), so P·SP/TP = L(2H+2Hkv)d·2 / (2L·2h·4) — exact, from the ledger."""
     cfg = c1.config
-    prompt = (c1_prompts()[0] * 2)[:64]
-    byts = {}
+    L, h, H, Hkv, d, P = cfg.n_layers, cfg.hidden, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, 2
+    M = 64
+    prompt = (c1_prompts()[0] * 2)[:M]
+    by = {}
     for mode in (ParallelMode.TP, ParallelMode.SP):
-        eng = make(c1, 2)
-        s = eng.new_sequence(0, capacity=64)
+        eng = make(c1, P)
+        s = eng.new_sequence(0, capacity=M)
         eng.step(Batch(BatchKind.PREFILL, [BatchItem(s, prompt)]), mode=mode)
-        byts[mode] = max(eng.group.device_bytes(d) for d in range(2))
-    assert byts[ParallelMode.SP] < byts[ParallelMode.TP]
+        by[mode] = [eng.group.ledger()[dev] for dev in range(P)]
+    frac = (P - 1) / P
+    for dev in range(P):
+        tp, sp = by[ParallelMode.TP][dev], by[ParallelMode.SP][dev]
+        assert tp["all_reduce"] == 2 * L * 2 * frac * M * h * 4
+        m_r = M // P
+        fwd = frac * m_r * (H + 2 * Hkv) * d * 2   # my tokens' q|k|v, every head block
+        back = frac * M * (H // P) * d * 2         # my head block, every token
+        assert sp["all_to_all"] == L * (fwd + back)
+        ratio = P * sp["all_to_all"] / tp["all_reduce"]
+        assert abs(ratio - L * (2 * H + 2 * Hkv) * d * 2 / (2 * L * 2 * h * 4)) < 1e-12
+        assert "all_to_all" not in tp and "all_reduce" not in sp
 
 
 def test_policy_threshold_and_mode_log(c1):
@@ -311,6 +327,28 @@ def test_swiftkv_matches_oracle(c1, mode):
                      mode=mode)
     olg, _ = oeng.step([(s, [t]) for s, t in zip(oseqs, toks)], prefill=False, mode=mode.value)
     assert rel_err(np.stack(to_np(lg)), np.stack(olg)) <= LOGIT_TOL
+
+
+@pytest.mark.parametrize("mode", [ParallelMode.TP, ParallelMode.SP])
+def test_swiftkv_band_and_cache_invariance(c1, mode):
+    """check_swiftkv_band (verify_checks.py:197-228): the metered FLOPs equal
+    the analytic count, the SwiftKV/standard ratio of a long prefill lies in
+    [0.50, 0.62] (cut = L/2), and the cache it leaves (fingerprint, bytes
+    written, every layer's K/V present) is the standard one."""
+    prompt = (c1_prompts()[0] * 4)[:300]
+    res = {}
+    for label, skv in (("std", None), ("skv", SwiftKvConfig(enabled=True, cut_layer=2))):
+        eng = make(c1, 2, swiftkv=skv)
+        s = eng.new_sequence(0, capacity=320)
+        batch = Batch(BatchKind.PREFILL, [BatchItem(s, prompt)])
+        shape = eng.pass_shape(batch)  # before the step commits the tokens
+        _, rec = eng.step(batch, mode=mode)
+        cut = None if skv is None else 2
+        assert rec.flops_per_device == flop_count(shape, mode, eng.config, 2, swiftkv_cut=cut)
+        res[label] = (sum(rec.flops_per_device), s.cache.fingerprint(), s.cache.write_counter)
+    ratio = res["skv"][0] / res["std"][0]
+    assert 0.50 <= ratio <= 0.62, ratio
+    assert res["skv"][1] == res["std"][1] and res["skv"][2] == res["std"][2]
 
 
 def test_compat_mode_against_reference_golden(golden):
