@@ -62,10 +62,28 @@ class PeerLinks:
             import torch.distributed as dist
             from . import ops
             buf = torch.zeros(total, dtype=torch.uint8, device=device)
+            # every step is collective and failure-tolerant, so either all ranks
+            # map their peers or all fall back to the NCCL collectives together
+            err = None
+            try:
+                mine = ops.ipc_export(buf)
+            except Exception as e:  # noqa: BLE001
+                mine, err = None, e
             handles: List = [None] * P
-            dist.all_gather_object(handles, ops.ipc_export(buf))
-            for r in range(P):
-                bases[r] = buf.data_ptr() if r == group.rank else ops.ipc_import(*handles[r])
+            dist.all_gather_object(handles, mine)
+            if err is None:
+                try:
+                    for r in range(P):
+                        if handles[r] is None:
+                            raise RuntimeError(f"rank {r} could not export its peer buffer")
+                        bases[r] = buf.data_ptr() if r == group.rank else ops.ipc_import(*handles[r])
+                except Exception as e:  # noqa: BLE001
+                    err = e
+            ok = torch.tensor([0 if err else 1], dtype=torch.int32,
+                              device=device if dist.get_backend() == "nccl" else "cpu")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 0:
+                raise RuntimeError(f"peer mapping failed ({err or 'on another rank'})")
             self._bufs = {group.rank: buf}
             self._views(group.rank, buf)
             torch.cuda.synchronize()
