@@ -1331,6 +1331,7 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
   const int sms = sm_count();
   const int64_t m_tiles = cdiv(M, BM);
   int bn = 256;
+  bool no_pair = false;
   if (swap_regime(M, N, sms)) {
     int rc = -1;
     if (M <= 32)
@@ -1348,20 +1349,35 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
     if (rc >= 0) return rc;
   }
   if (m_tiles * cdiv(N, 256) < sms && epilogue != SP_EPI_SWIGLU) {
-    bn = 32;
-    for (int c : {128, 64}) {
-      if (m_tiles * cdiv(N, c) >= sms) {
-        bn = c;
-        break;
+    // fewer 128x256 tiles than SMs: pick the tile by a wave model — cost =
+    // waves x per-SM tile work (relative to half a 256x256 pair tile) x the
+    // measured per-SM efficiency loss of 1-CTA tiles vs 2-CTA pairs
+    // (tools/gemm_sweep.py: ~1.3 for 128x256/128x128, ~1.7 for 128x64,
+    // ~2.5 for 128x32).  All candidates share the K loop: bit-identical.
+    const bool pair_ok = M >= 256 && N % 256 == 0;
+    double best = pair_ok ? (double)cdiv(cdiv(M, 256) * cdiv(N, 256), sms / 2) : 1e30;
+    bn = 256;
+    bool use_pair = pair_ok;
+    const struct { int bn; double f; } cands[] = {{256, 1.3}, {128, 1.3}, {64, 1.7}, {32, 2.5}};
+    for (const auto& c : cands) {
+      const double cost = (double)cdiv(m_tiles * cdiv(N, c.bn), sms) * (c.bn / 256.0) * c.f;
+      if (cost < best) {
+        best = cost;
+        bn = c.bn;
+        use_pair = false;
       }
     }
+    no_pair = !use_pair;
   }
   if (epilogue == SP_EPI_PARTIAL_F32) epilogue = SP_EPI_STORE_F32;  // one "partial" = the result
   if (const char* f = getenv("SP_GEMM_FORCE_BN")) {
     const int fb = atoi(f);
-    if ((fb == 32 || fb == 64 || fb == 128 || fb == 256) && epilogue != SP_EPI_SWIGLU) bn = fb;
+    if ((fb == 32 || fb == 64 || fb == 128 || fb == 256) && epilogue != SP_EPI_SWIGLU) {
+      bn = fb;
+      no_pair = false;
+    }
   }
-  if (bn == 256 && M >= 256 && N % 256 == 0) {
+  if (bn == 256 && M >= 256 && N % 256 == 0 && !no_pair) {
     const char* e = getenv("SP_GEMM_2CTA");
     if (!(e && e[0] == '0'))
       return launch_pair(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
