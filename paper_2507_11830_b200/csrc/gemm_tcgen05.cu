@@ -1352,13 +1352,13 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
     // fewer 128x256 tiles than SMs: pick the tile by a wave model — cost =
     // waves x per-SM tile work (relative to half a 256x256 pair tile) x the
     // measured per-SM efficiency loss of 1-CTA tiles vs 2-CTA pairs
-    // (tools/gemm_sweep.py: ~1.3 for 128x256/128x128, ~1.7 for 128x64,
+    // (tools/gemm_sweep.py: ~1.3 for 128x256, ~1.4 for 128x128, ~1.7 for 128x64,
     // ~2.5 for 128x32).  All candidates share the K loop: bit-identical.
     const bool pair_ok = M >= 256 && N % 256 == 0;
     double best = pair_ok ? (double)cdiv(cdiv(M, 256) * cdiv(N, 256), sms / 2) : 1e30;
     bn = 256;
     bool use_pair = pair_ok;
-    const struct { int bn; double f; } cands[] = {{256, 1.3}, {128, 1.3}, {64, 1.7}, {32, 2.5}};
+    const struct { int bn; double f; } cands[] = {{256, 1.3}, {128, 1.4}, {64, 1.7}, {32, 2.5}};
     for (const auto& c : cands) {
       const double cost = (double)cdiv(m_tiles * cdiv(N, c.bn), sms) * (c.bn / 256.0) * c.f;
       if (cost < best) {
