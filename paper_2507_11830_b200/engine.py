@@ -226,10 +226,13 @@ def attention_split_plan(wl, spans, hist, tt: int, hk: int, sms: int, max_slots:
         q_end = min(t0 + tt, spans[i])
         tiles.append((i, t0, -(-(hist[i] + q_end) // kt)))
     total = sum(c for _, _, c in tiles)
-    # one wave: pieces of at most total/SMs key tiles, longest first (the
-    # block scheduler then packs them LPT-style); measured better than two
-    # waves of smaller pieces (per-CTA prologue, Q reload, partial traffic)
-    chunk = max(2, -(-total // max(1, sms // hk)))
+    # ~1.5 waves: pieces of at most total/(1.5 SMs) key tiles, longest first
+    # (the block scheduler then packs them LPT-style).  SP=8 8K attention
+    # (tools/attn_sp_shapes.py): 1 wave 750, 1.25 770, 1.5 800, 1.75 774,
+    # 2 673 TFLOP/s — smaller pieces pack better until the per-CTA prologue,
+    # Q reload and partial traffic dominate.  SP_ATTN_SPLIT_WAVES overrides.
+    waves = float(os.environ.get("SP_ATTN_SPLIT_WAVES", "1.5"))
+    chunk = max(2, -(-total // max(1, int(waves * sms) // hk)))
     entries, combine, slot = [], [], 0
     for i, t0, c in tiles:
         ns = -(-c // chunk)

@@ -8,6 +8,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2507_11830_b200 import ops  # noqa: E402
+from paper_2507_11830_b200.engine import attention_split_plan  # noqa: E402
 
 T, d, bs = 8192, 128, 64
 for N in [int(x) for x in sys.argv[1:]] or [1, 2, 4, 8]:
@@ -32,23 +33,15 @@ for N in [int(x) for x in sys.argv[1:]] or [1, 2, 4, 8]:
                       head_dim=d, block_size=bs, ws=ws)
     # the engine's split-KV plan (Engine._split_plan) when the tiles do not fill the SMs
     sms = torch.cuda.get_device_properties(0).multi_processor_count
-    if len(wl) * hk < sms and os.environ.get("SP_ATTN_SPLIT") != "0":
-        tiles = [(i, t0, -(-(t0 + min(tt, T - t0)) // 128)) for i, t0 in wl]
-        chunk = max(2, -(-sum(c for _, _, c in tiles) // max(1, sms // hk)))
-        ent, comb, slot = [], [], 0
-        for i, t0, c in tiles:
-            ns = -(-c // chunk)
-            if ns <= 1:
-                ent.append((c, i, t0, 0, c, -1))
-                continue
-            b = [c * k // ns for k in range(ns + 1)]
-            for k in range(ns):
-                ent.append((b[k + 1] - b[k], i, t0, b[k], b[k + 1], slot + k))
-            comb.append((i, t0, slot, ns))
-            slot += ns
-        ent.sort(key=lambda e: -e[0])
-        T32 = lambda a: torch.tensor(a, dtype=torch.int32, device="cuda").view(-1)
-        w2, sp2, cb2 = T32([(e[1], e[2]) for e in ent]), T32([(e[3], e[4], e[5], 0) for e in ent]), T32(comb)
+    plan = None
+    if os.environ.get("SP_ATTN_SPLIT") != "0":
+        wl3 = [(i, t0, t0) for i, t0 in wl]
+        plan = attention_split_plan(wl3, [T], [0], tt, hk, sms, 1 << 30)
+    if plan is not None:
+        work_np, split_np, comb_np, slot = plan
+        T32 = lambda a: torch.from_numpy(a).to(device="cuda").view(-1)  # noqa: E731
+        w2, sp2, cb2 = T32(work_np), T32(split_np), T32(comb_np)
+        ent, comb = work_np, comb_np
         ws = torch.empty(slot * hk * ops.SPLIT_SLOT_BYTES // 4 + 1, device="cuda")
 
         def fn():
