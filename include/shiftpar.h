@@ -68,12 +68,15 @@ sp_status sp_device_check(int* sm_count);
  *    D + (n / peer_width) * peer_stride + m * ldd + (n % peer_width)
  *    (the per-peer contiguous send layout of the SP seq->head all-to-all,
  *    i.e. the pack fused into the epilogue).
- * Fixed tiling: for M > 128 each D element is one ascending-K reduction
- * independent of M and of the N window -> row/column splits are bit-exact
- * (the property of tensor_core.py:1-28 the SP path relies on).  For M <= 128
- * (decode) the weight is streamed swap-AB over 256-row super tiles with K
- * split just enough to cover the SMs; split partials are summed in ascending
- * split order (deterministic within the regime).
+ * Fixed tiling: outside the decode regime each D element is one
+ * ascending-K reduction independent of M, of the N window and of the tile
+ * shape chosen (2-CTA 256x256 pairs or 1-CTA 128x{256,128,64,32}, picked by a
+ * wave model) -> row/column splits are bit-exact (the property of
+ * tensor_core.py:1-28 the SP path relies on).  Decode regime (M <= 256 and
+ * fewer 256-row weight super tiles than SMs): the weight is streamed swap-AB
+ * over 256-row super tiles (tokens padded to 32/64/128/256) with K split just
+ * enough to cover the SMs; split partials are summed in ascending split order
+ * (deterministic within the regime; SP_GEMM_NO_SPLITK=1 disables it).
  */
 sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_chunk_stride,
                        const void* B, int64_t ldb, void* D, int64_t ldd, int M, int N, int K,
