@@ -86,6 +86,19 @@ sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
  * the epilogue.  NULL disables split-K.  Results are identical within a
  * regime; across regimes they differ at f32 rounding level. */
 sp_status sp_gemm_set_workspace(void* ws, int64_t bytes);
+/* QKV projection with RoPE and the paged KV write fused into the epilogue
+ * (parallel_engine.py:359-361 QKV matmul + kv_cache.py:99-122 append, with the
+ * build's rotary embedding): the [M, (q_heads + 2 kv_heads) * 128] product of
+ * A [M, K] and B [N, K] is never stored; q heads are rotated into q_out
+ * (row stride ldq), k heads rotated and v heads copied into the pools at
+ * slot[m] (slot < 0: skipped) exactly as sp_rope_kv_write lays them out.
+ * head_dim 128; rope_table NULL = no rotation.  Bit-identical to
+ * sp_gemm_bf16(SP_EPI_STORE_BF16) followed by sp_rope_kv_write. */
+sp_status sp_gemm_bf16_qkv_rope(const void* A, int64_t lda, const void* B, int64_t ldb, int M,
+                                int K, const int32_t* pos, const int32_t* slot,
+                                const float* rope_table, void* q_out, int64_t ldq, void* k_pool,
+                                void* v_pool, int q_heads, int kv_heads, int block_size,
+                                void* stream);
 /* Number of f32 [M][N] partial slabs SP_EPI_PARTIAL_F32 writes for this shape
  * (1 outside the split-K regime).  Host-only, deterministic. */
 int sp_gemm_partials(int M, int N, int K);

@@ -50,6 +50,8 @@ SIGNATURES = {
                                            _c_int, _c_int, _c_int, _c_int, _c_int, _vp]),
     "sp_rope_kv_write": (_c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _c_int, _c_int,
                                   _c_int, _c_int, _c_int, _vp]),
+    "sp_gemm_bf16_qkv_rope": (_c_int, [_vp, _i64, _vp, _i64, _c_int, _c_int, _vp, _vp, _vp, _vp,
+                                       _i64, _vp, _vp, _c_int, _c_int, _c_int, _vp]),
     "sp_attention": (_c_int, [_vp, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _c_int,
                               _vp, _c_int, _c_int, _c_int, _vp, _i64, _c_int, _c_int, _c_int,
                               _c_int, _vp, _i64, _vp]),

@@ -54,6 +54,15 @@ inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// RoPE rotation of one (x_i, x_{i+d/2}) pair, rounding explicit (no FMA
+// contraction) so the standalone RoPE kernel and the GEMM epilogue that fuses
+// it produce identical bits: (a cos - b sin, b cos + a sin).
+__device__ __forceinline__ void rope_rotate(float a, float b, float c, float s, float& na,
+                                            float& nb) {
+  na = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, s));
+  nb = __fadd_rn(__fmul_rn(b, c), __fmul_rn(a, s));
+}
+
 // ------------------------------------------------------------ small utils
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

@@ -71,7 +71,23 @@ struct Params {
   // peer_ptrs[b] at row (m + peer_row_off) — stores cross NVLink directly
   const unsigned long long* peer_ptrs;
   int64_t peer_row_off;
+  // EPI_QKV_ROPE (sp_gemm_bf16_qkv_rope): columns are [q heads | k heads | v
+  // heads] x 128; q rotated -> q_out, k rotated -> k_pool, v -> v_pool at the
+  // row's cache slot (the work of rope_kv_kernel, fused into the epilogue)
+  struct Rope {
+    const float* table;  // [pos][64] (cos, sin) pairs
+    const int32_t* pos;
+    const int32_t* slot;
+    __nv_bfloat16* q_out;
+    int64_t ldq;
+    __nv_bfloat16* k_pool;
+    __nv_bfloat16* v_pool;
+    int q_heads, kv_heads, block_size;
+  } rope;
 };
+
+constexpr int EPI_QKV_ROPE = 100;  // internal: only via sp_gemm_bf16_qkv_rope
+static thread_local Params::Rope t_rope = {};
 
 // destination element (m, n) of D honouring the per-peer layouts
 template <typename T>
@@ -89,6 +105,71 @@ __device__ __forceinline__ T* out_ptr(const Params& p, int m, int64_t n) {
     }
   }
   return base + off + row * p.ldd + col;
+}
+
+// EPI_QKV_ROPE for one accumulator row (token m) over the 256 columns
+// [n0, n0 + 256) = two 128-wide heads.  Values are rounded to bf16 first and
+// rotated with rope_rotate, exactly what rope_kv_kernel does with the bf16
+// qkv the plain epilogue would have stored.  tcgen05.ld is warp-collective:
+// every lane loads, only valid rows store.
+__device__ __forceinline__ void qkv_rope_row(const Params& p, int m, int n0, uint32_t tb) {
+  const Params::Rope& R = p.rope;
+  const bool valid = m < p.M;
+  int pos = 0, slot = -1;
+  if (valid) {
+    pos = R.pos[m];
+    slot = R.slot ? R.slot[m] : -1;
+  }
+#pragma unroll 1
+  for (int hh = 0; hh < 2; ++hh) {
+    const int h = (n0 >> 7) + hh;
+    __nv_bfloat16* dst = nullptr;
+    bool rotate = false;
+    if (h < R.q_heads) {
+      dst = R.q_out ? R.q_out + (int64_t)m * R.ldq + (int64_t)h * 128 : nullptr;
+      rotate = R.table != nullptr;
+    } else if (slot >= 0 && h < R.q_heads + 2 * R.kv_heads) {
+      const int kv = h - R.q_heads;
+      const int kvh = kv % R.kv_heads;
+      __nv_bfloat16* pool = kv < R.kv_heads ? R.k_pool : R.v_pool;
+      const int64_t blk = slot / R.block_size, off = slot % R.block_size;
+      dst = pool + ((blk * R.kv_heads + kvh) * R.block_size + off) * 128;
+      rotate = R.table != nullptr && kv < R.kv_heads;
+    }
+#pragma unroll 1
+    for (int c = 0; c < 64; c += 32) {
+      uint32_t ra[32], rb[32];
+      tmem_ld32(tb + hh * 128 + c, ra);
+      tmem_ld32(tb + hh * 128 + 64 + c, rb);
+      tmem_ld_wait();
+      if (!valid || dst == nullptr) continue;
+      uint32_t oa[16], ob[16];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        // the bf16 rounding the plain epilogue applies before rope_kv_kernel reads it
+        const float2 a = unpack_bf16x2(pack_bf16x2(__uint_as_float(ra[j]), __uint_as_float(ra[j + 1])));
+        const float2 b = unpack_bf16x2(pack_bf16x2(__uint_as_float(rb[j]), __uint_as_float(rb[j + 1])));
+        if (rotate) {
+          const float4 cs = *reinterpret_cast<const float4*>(R.table + ((int64_t)pos * 64 + c + j) * 2);
+          float na0, nb0, na1, nb1;
+          rope_rotate(a.x, b.x, cs.x, cs.y, na0, nb0);
+          rope_rotate(a.y, b.y, cs.z, cs.w, na1, nb1);
+          oa[j / 2] = pack_bf16x2(na0, na1);
+          ob[j / 2] = pack_bf16x2(nb0, nb1);
+        } else {
+          oa[j / 2] = pack_bf16x2(a.x, a.y);
+          ob[j / 2] = pack_bf16x2(b.x, b.y);
+        }
+      }
+      uint4* da = reinterpret_cast<uint4*>(dst + c);
+      uint4* db = reinterpret_cast<uint4*>(dst + 64 + c);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        da[q] = make_uint4(oa[4 * q], oa[4 * q + 1], oa[4 * q + 2], oa[4 * q + 3]);
+        db[q] = make_uint4(ob[4 * q], ob[4 * q + 1], ob[4 * q + 2], ob[4 * q + 3]);
+      }
+    }
+  }
 }
 
 __device__ __forceinline__ void tile_coords(int t, const Params& p, int& mb, int& nb) {
@@ -346,6 +427,8 @@ __global__ void __launch_bounds__(NUM_THREADS, Tile<BN_>::MIN_BLOCKS)
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
           store_chunk(q, m, nb * BN + c, v, SP_EPI_STORE_F32, p.N);
         }
+      } else if (BN == 256 && p.epi == EPI_QKV_ROPE) {
+        qkv_rope_row(p, m, nb * 256, tb);
       } else if (p.epi == SP_EPI_SWIGLU) {
 #pragma unroll 1
         for (int c = 0; c < BN / 2; c += 32) {
@@ -848,7 +931,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * 256;
       const int m = mb * 256 + rank * 128 + row;
-      if (p.epi == SP_EPI_SWIGLU) {
+      if (p.epi == EPI_QKV_ROPE) {
+        qkv_rope_row(p, m, nb * 256, tb);
+      } else if (p.epi == SP_EPI_SWIGLU) {
 #pragma unroll 1
         for (int c = 0; c < 128; c += 32) {
           uint32_t g[32], u[32];
@@ -1073,6 +1158,7 @@ static int launch(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_chunk_
   Params p;
   p.peer_ptrs = t_peer_ptrs;
   p.peer_row_off = t_peer_row_off;
+  p.rope = t_rope;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -1182,6 +1268,7 @@ static int launch_swap(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   Params p;
   p.peer_ptrs = t_peer_ptrs;
   p.peer_row_off = t_peer_row_off;
+  p.rope = t_rope;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -1243,6 +1330,7 @@ static int launch_pair(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   Params p;
   p.peer_ptrs = t_peer_ptrs;
   p.peer_row_off = t_peer_row_off;
+  p.rope = t_rope;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -1389,6 +1477,39 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
     case 64: return launch<64>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue, peer_width, peer_stride, stream);
     default: return launch<32>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue, peer_width, peer_stride, stream);
   }
+}
+
+// QKV projection with RoPE + paged KV write fused into the epilogue
+// (prefill-size M): 256-column tiles = two whole heads, so every rotation
+// pair (i, i + 64) sits in one thread's accumulator row.  Bit-identical to
+// sp_gemm_bf16(EPI_STORE_BF16) followed by sp_rope_kv_write.
+extern "C" sp_status sp_gemm_bf16_qkv_rope(const void* A, int64_t lda, const void* B, int64_t ldb,
+                                           int M, int K, const int32_t* pos, const int32_t* slot,
+                                           const float* rope_table, void* q_out, int64_t ldq,
+                                           void* k_pool, void* v_pool, int q_heads, int kv_heads,
+                                           int block_size, void* stream) {
+  using namespace sp::gemm;
+  const int N = (q_heads + 2 * kv_heads) * 128;
+  if (M < 0 || K <= 0 || q_heads <= 0 || kv_heads < 0 || block_size <= 0)
+    return fail(kInvalid, "gemm_qkv_rope: bad shape");
+  if (M == 0) return kOk;
+  if (!A || !B || !pos || (kv_heads > 0 && (!k_pool || !v_pool || !slot)))
+    return fail(kInvalid, "gemm_qkv_rope: null pointer");
+  if (N % 256) return fail(kUnsupported, "gemm_qkv_rope: q_heads + 2 kv_heads must be even");
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15 || lda % 8 || ldb % 8 ||
+      ldq % 8)
+    return fail(kInvalid, "gemm_qkv_rope: 16-byte aligned operands and rows required");
+  t_rope = Params::Rope{rope_table, pos, slot, static_cast<__nv_bfloat16*>(q_out), ldq,
+                        static_cast<__nv_bfloat16*>(k_pool), static_cast<__nv_bfloat16*>(v_pool),
+                        q_heads, kv_heads, block_size};
+  int rc;
+  const char* e = getenv("SP_GEMM_2CTA");
+  if (M >= 256 && !(e && e[0] == '0'))
+    rc = launch_pair(A, lda, 0, 0, B, ldb, q_out, ldq, M, N, K, EPI_QKV_ROPE, 0, 0, stream);
+  else
+    rc = launch<256>(A, lda, 0, 0, B, ldb, q_out, ldq, M, N, K, EPI_QKV_ROPE, 0, 0, stream);
+  t_rope = Params::Rope{};
+  return rc;
 }
 
 extern "C" sp_status sp_gemm_bf16_to_peers(const void* A, int64_t lda, int64_t a_kchunk,

@@ -214,8 +214,9 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, const floa
       const float4 c2 = cs[q];  // (cos, sin) of pairs i0+2q and i0+2q+1
       const float2 a = unpack_bf16x2(pa[q]);
       const float2 b = unpack_bf16x2(pb[q]);
-      const float na0 = a.x * c2.x - b.x * c2.y, nb0 = b.x * c2.x + a.x * c2.y;
-      const float na1 = a.y * c2.z - b.y * c2.w, nb1 = b.y * c2.z + a.y * c2.w;
+      float na0, nb0, na1, nb1;
+      rope_rotate(a.x, b.x, c2.x, c2.y, na0, nb0);
+      rope_rotate(a.y, b.y, c2.z, c2.w, na1, nb1);
       pa[q] = pack_bf16x2(na0, na1);
       pb[q] = pack_bf16x2(nb0, nb1);
     }

@@ -207,6 +207,14 @@ class _GraphEntry:
         self.failed = False  # capture raised: this key stays eager
 
 
+class _RopedQ:
+    """Marker: the QKV epilogue already rotated q (here) and wrote K/V."""
+    __slots__ = ("q",)
+
+    def __init__(self, q: torch.Tensor):
+        self.q = q
+
+
 def attention_split_plan(wl, spans, hist, tt: int, hk: int, sms: int, max_slots: int):
     """Split-KV plan for a prefill pass whose work tiles x kv heads do not
     fill the SMs (one long request under SP=8: 128 tiles x 1 kv head with
@@ -317,6 +325,7 @@ class Engine:
         self._sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         self.cuda_graphs = cuda_graphs
         self._fuse_splitk = os.environ.get("SP_FUSE_SPLITK", "1") != "0"
+        self._fuse_rope = os.environ.get("SP_FUSE_ROPE", "1") != "0"
         self._graphs: Dict[tuple, _GraphEntry] = {}
         self._graph_pool = torch.cuda.graph_pool_handle() if cuda_graphs else None
         self._capturing = False
@@ -666,6 +675,20 @@ class Engine:
                           kv_heads=cfg.kv_heads // P, head_dim=cfg.head_dim,
                           block_size=self.pool.block_size)
 
+    def _fused_qkv_rope(self, M: int, hq: int, hk: int) -> bool:
+        """QKV GEMM with RoPE + KV write in its epilogue: prefill-size passes
+        (the decode regime keeps its K-split partials -> RoPE kernel), head_dim
+        128, whole-head 256-column tiles.  SP_FUSE_ROPE=0 disables."""
+        return (M > 256 and self.config.head_dim == 128 and (hq + 2 * hk) % 2 == 0
+                and self._fuse_rope)
+
+    def _qkv_rope(self, r, layer, xn, wqkv, q, meta, hq, hk, meter) -> None:
+        h = self.config.hidden
+        ops.gemm_qkv_rope(xn, wqkv, M=meta.M, K=h, lda=h, ldb=h, pos=meta.pos, slot=meta.slots,
+                          rope=self.weights.rope, q_out=q, k_pool=self.pool.layer_k(r, layer),
+                          v_pool=self.pool.layer_v(r, layer), q_heads=hq, kv_heads=hk,
+                          block_size=self.pool.block_size, meter=meter)
+
     def _stage_all(self, layer: int, batch: Batch) -> None:
         # every process tracks the global cursors: all P devices append this layer
         if self._capturing:
@@ -725,6 +748,9 @@ class Engine:
                     ops.gemm(xn, lw.wqkv[r * W:(r + 1) * W], qparts, ops.EPI_PARTIAL_F32, M=M,
                              N=W, K=h, lda=h, ldb=h, ldd=W, meter=meters[r])
                     self._kv_write(r, layer, None, q, meta, batch, parts=(qparts, n_qkv))
+                elif self._fused_qkv_rope(M, hq, hk):
+                    self._qkv_rope(r, layer, xn, lw.wqkv[r * W:(r + 1) * W], q, meta, hq, hk,
+                                   meters[r])
                 else:
                     qkv = torch.empty((M, W), dtype=torch.bfloat16, device=dev)
                     ops.gemm(xn, lw.wqkv[r * W:(r + 1) * W], qkv, ops.EPI_STORE_BF16, M=M, N=W,
@@ -951,7 +977,7 @@ class Engine:
         cfg, w, g = self.config, self.weights, self.group
         P = self.world_size
         M, h, d = meta.M, cfg.hidden, cfg.head_dim
-        hq = cfg.n_heads // P
+        hq, hk = cfg.n_heads // P, cfg.kv_heads // P
         W = w.qkv_width
         hqw = hq * d
         dev, eps = self.device, cfg.norm_eps
@@ -991,6 +1017,10 @@ class Engine:
                         ops.gemm(xn, lw.wqkv, qparts, ops.EPI_PARTIAL_F32, M=M, N=W, K=h,
                                  lda=h, ldb=h, ldd=W, meter=meters[r])
                         recv[r] = (qparts, n_qkv)
+                    elif self._fused_qkv_rope(M, hq, hk):
+                        qf = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
+                        self._qkv_rope(r, layer, xn, lw.wqkv, qf, meta, hq, hk, meters[r])
+                        recv[r] = _RopedQ(qf)
                     else:
                         send[r] = torch.empty((M, W), dtype=torch.bfloat16, device=dev)
                         ops.gemm(xn, lw.wqkv, send[r], ops.EPI_STORE_BF16, M=M, N=W, K=h, lda=h,
@@ -1013,11 +1043,14 @@ class Engine:
             self._stage_all(layer, batch)
             att = {}
             for r in g.local_ranks:
-                q = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
-                if isinstance(recv[r], tuple):
-                    self._kv_write(r, layer, None, q, meta, batch, parts=recv[r])
+                if isinstance(recv[r], _RopedQ):  # RoPE + KV write done in the QKV epilogue
+                    q = recv[r].q
                 else:
-                    self._kv_write(r, layer, recv[r], q, meta, batch)
+                    q = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
+                    if isinstance(recv[r], tuple):
+                        self._kv_write(r, layer, None, q, meta, batch, parts=recv[r])
+                    else:
+                        self._kv_write(r, layer, recv[r], q, meta, batch)
                 o = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
                 self._attend(r, layer, q, o, meta, meters[r])
                 att[r] = o

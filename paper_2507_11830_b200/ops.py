@@ -111,6 +111,28 @@ def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, epilogue: int, *, M:
     _lib.check(rc, "sp_gemm_bf16")
 
 
+def gemm_qkv_rope(a: torch.Tensor, b: torch.Tensor, *, M: int, K: int, lda: int, ldb: int,
+                  pos: torch.Tensor, slot: torch.Tensor, rope: Optional[torch.Tensor],
+                  q_out: Optional[torch.Tensor], k_pool: torch.Tensor, v_pool: torch.Tensor,
+                  q_heads: int, kv_heads: int, block_size: int, meter=None) -> None:
+    """QKV projection with RoPE + paged KV write in the epilogue (head_dim 128):
+    bit-identical to gemm(EPI_STORE_BF16) followed by rope_kv_write."""
+    _need(a, torch.bfloat16, "gemm A")
+    _need(b, torch.bfloat16, "gemm B")
+    N = (q_heads + 2 * kv_heads) * 128
+    if meter is not None:
+        meter.add_matmul(M, K, N)
+    if M == 0:
+        return
+    nbytes = (M * K + N * K) * 2 + M * N * 2
+    with _Timed("gemm", 2 * M * N * K, nbytes):
+        rc = _lib.load().sp_gemm_bf16_qkv_rope(
+            a.data_ptr(), lda, b.data_ptr(), ldb, M, K, pos.data_ptr(), slot.data_ptr(),
+            _ptr(rope), _ptr(q_out), 0 if q_out is None else q_out.stride(0), k_pool.data_ptr(),
+            v_pool.data_ptr(), q_heads, kv_heads, block_size, _stream())
+    _lib.check(rc, "sp_gemm_bf16_qkv_rope")
+
+
 _gemm_ws: Optional[torch.Tensor] = None
 
 

@@ -377,6 +377,27 @@ def d128():
 
 
 @pytest.mark.parametrize("mode", [ParallelMode.TP, ParallelMode.SP])
+def test_fused_qkv_rope_prefill_bitexact(d128, mode, monkeypatch):
+    """Prefill passes (M > 256) run the QKV projection with RoPE + KV write in
+    the GEMM epilogue; logits and the cache equal the unfused path bit for bit."""
+    prompts = [(c1_prompts()[i] * 3)[:n] for i, n in ((0, 200), (1, 150))]
+    res = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("SP_FUSE_ROPE", fused)
+        for p in (1, 2):
+            eng = make(d128, p)
+            seqs = [eng.new_sequence(i, capacity=400) for i in range(2)]
+            lg, _ = eng.step(Batch(BatchKind.PREFILL, [BatchItem(s, q) for s, q in
+                                                       zip(seqs, prompts)]), mode=mode)
+            k0 = seqs[0].cache.read_window(0, 1, 0)[0] if p == 1 else None
+            res[(fused, p)] = ([x.cpu() for x in lg], k0)
+    for p in (1, 2):
+        for a, b in zip(res[("1", p)][0], res[("0", p)][0]):
+            assert torch.equal(a, b), p
+    assert torch.equal(res[("1", 1)][1], res[("0", 1)][1])
+
+
+@pytest.mark.parametrize("mode", [ParallelMode.TP, ParallelMode.SP])
 def test_head_dim_128_tcgen05_attention_matches_oracle(d128, mode):
     rng = np.random.default_rng(5)
     prompts = [[int(t) for t in rng.integers(0, 512, size=n)] for n in (300, 17, 129)]

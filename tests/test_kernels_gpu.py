@@ -502,6 +502,43 @@ def test_peer_allreduce_from_partial_slabs_bitexact(P, M, N, K):
         ops.set_gemm_workspace(None)
 
 
+@pytest.mark.parametrize("M,hq,hk,pair", [(300, 32, 8, "1"), (1000, 4, 1, "1"), (1000, 4, 1, "0"),
+                                         (200, 8, 2, "1"), (2048, 16, 4, "1")])
+def test_gemm_qkv_rope_fused_bitexact(M, hq, hk, pair, monkeypatch):
+    """QKV GEMM with RoPE + paged KV write in its epilogue (2-CTA pairs or the
+    1-CTA 128x256 tile) == GEMM(bf16) then rope_kv_write, bit for bit; rows
+    with slot -1 write no K/V."""
+    monkeypatch.setenv("SP_GEMM_2CTA", pair)
+    from paper_2507_11830_b200.weights import rope_table
+    d, bs, K = 128, 64, 1024
+    W = (hq + 2 * hk) * d
+    a, w = rnd(M, K, seed=90), rnd(W, K, seed=91, scale=0.05)
+    pos = (torch.arange(M, dtype=torch.int32, device="cuda") * 7) % 4000
+    nblk = -(-M // bs) + 4
+    slot = torch.randperm(nblk * bs, device="cuda")[:M].to(torch.int32)
+    slot[::17] = -1
+    tab = torch.from_numpy(rope_table(4096, d, 500000.0, None)).cuda()
+    res = []
+    for fused in (True, False):
+        kp = torch.zeros(nblk, hk, bs, d, device="cuda", dtype=torch.bfloat16)
+        vp = torch.zeros_like(kp)
+        q = torch.zeros(M, hq * d, device="cuda", dtype=torch.bfloat16)
+        if fused:
+            ops.gemm_qkv_rope(a, w, M=M, K=K, lda=K, ldb=K, pos=pos, slot=slot, rope=tab, q_out=q,
+                              k_pool=kp, v_pool=vp, q_heads=hq, kv_heads=hk, block_size=bs)
+        else:
+            qkv = torch.empty(M, W, device="cuda", dtype=torch.bfloat16)
+            monkeypatch.setenv("SP_GEMM_NO_SPLITK", "1")  # the same (non-swap) GEMM regime
+            ops.gemm(a, w, qkv, ops.EPI_STORE_BF16, M=M, N=W, K=K, lda=K, ldb=K, ldd=W)
+            monkeypatch.delenv("SP_GEMM_NO_SPLITK")
+            ops.rope_kv_write(qkv, pos, slot, tab, q, kp, vp, rows=M, q_heads=hq, kv_heads=hk,
+                              head_dim=d, block_size=bs)
+        res.append((q, kp, vp))
+    for x, y in zip(res[0], res[1]):
+        assert torch.equal(x, y)
+    assert res[0][1].abs().sum() > 0 and res[0][2].abs().sum() > 0
+
+
 def test_rope_kv_write_from_partials_bitexact():
     """QKV projection left as K-split partials, reduced inside RoPE + KV write,
     equals the bf16 projection (reduced by the GEMM) fed to RoPE + KV write."""
