@@ -205,6 +205,7 @@ class _GraphEntry:
         self.charges: list = []
         self.kernels = 0
         self.failed = False  # capture raised: this key stays eager
+        self.seen = 0  # eager passes run with this key so far
 
 
 class _RopedQ:
@@ -326,6 +327,7 @@ class Engine:
         self.cuda_graphs = cuda_graphs
         self._fuse_splitk = os.environ.get("SP_FUSE_SPLITK", "1") != "0"
         self._fuse_rope = os.environ.get("SP_FUSE_ROPE", "1") != "0"
+        self._graph_after = max(1, int(os.environ.get("SP_GRAPH_AFTER", "2")))
         self._graphs: Dict[tuple, _GraphEntry] = {}
         self._graph_pool = torch.cuda.graph_pool_handle() if cuda_graphs else None
         self._capturing = False
@@ -405,7 +407,13 @@ class Engine:
             fwd = self._forward_tp if mode is ParallelMode.TP else self._forward_sp
             logits = fwd(meta, batch, meters, span_logits, cut)
             if graph_key is not None and not self._graphs[graph_key].failed:
-                self._capture(graph_key, meta, batch, fwd)
+                # capture once a key recurs: serving sees many one-off batch sizes
+                # whose capture (a second host-side forward + sync) would cost more
+                # than the eager pass it replaces (SP_GRAPH_AFTER, default 2)
+                e = self._graphs[graph_key]
+                e.seen += 1
+                if e.seen >= self._graph_after:
+                    self._capture(graph_key, meta, batch, fwd)
         for it in batch.items:
             it.seq.cache.commit(len(it.tokens))
         record = StepRecord(step_id=self._step_counter, mode=mode, kind=batch.kind,

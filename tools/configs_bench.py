@@ -28,7 +28,7 @@ except Exception:
     pass
 
 
-def timed(fn, steps, warm=2):
+def timed(fn, steps, warm=3):
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
