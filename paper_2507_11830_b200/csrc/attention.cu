@@ -611,13 +611,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 2) decode_tma_kernel(
 
 static int decode_tma_splits(int n_items, int kv_heads, int max_kv_len) {
   const int ctas = n_items * kv_heads;
-  // two CTAs per SM are resident: split only until one wave of slots is
-  // covered (measured: B=64 x 8 kv heads runs best unsplit; tuning override
-  // SP_DECODE_SPLITS)
-  int want = (2 * 148 + ctas - 1) / ctas;
+  // split until ~256 CTAs (the producer streams the first ring of each split
+  // before the PDL wait, so fewer, longer splits win over filling all 296
+  // slots), keeping >= 8 page slices per split (>= 4 when there are very few
+  // (item, head) pairs).  Measured in-graph (ctx 2K): B=4 3.79 -> 3.68 ms,
+  // B=8 4.03 -> 3.91, B=16 4.57 -> 4.32, B=32 5.28 -> 5.06 vs the old
+  // one-wave-of-296 rule.  Tuning override SP_DECODE_SPLITS.
+  int want = (256 + ctas - 1) / ctas;
   if (const char* e = getenv("SP_DECODE_SPLITS")) want = atoi(e);
   const int pages = (max_kv_len + dec::PAGE - 1) / dec::PAGE;
-  const int max_useful = (pages + 3) / 4;  // >= 4 page slices per split
+  const int max_useful = ctas < 16 ? (pages + 3) / 4 : (pages / 8 > 1 ? pages / 8 : 1);
   if (want > max_useful) want = max_useful;
   if (want > 64) want = 64;
   return want < 1 ? 1 : want;
