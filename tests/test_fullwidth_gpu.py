@@ -1,6 +1,7 @@
-"""Parity at the BASELINE model width: Llama-3.1-8B geometry
+"""Parity at the BASELINE model widths: Llama-3.1-8B geometry
 (h 4096, 32q/8kv heads of 128, f 14336, V 128256) at truncated depth (2
-layers) against the fp32 oracle on the same bf16 weights, and size-independent
+layers) and Llama-3.3-70B layer geometry (h 8192, 64q/8kv, f 28672) at one
+layer, against the fp32 oracle on the same bf16 weights, and size-independent
 properties at the full 8K bench size."""
 
 import numpy as np
@@ -47,6 +48,33 @@ def test_8b_width_prefill_and_decode_vs_oracle(w8b_l2, mode):
     tok = int(np.argmax(want[-1]))
     lg, _ = eng.step(Batch(BatchKind.DECODE, [BatchItem(s, [tok])]), mode=mode)
     want2, _ = oracle.forward_reference(w8b_l2, prompt + [tok])
+    assert rel_err(lg[0].cpu().numpy(), want2[-1]) <= LOGIT_TOL
+
+
+@pytest.fixture(scope="module")
+def w70b_l1():
+    # Llama-3.3-70B layer geometry (h 8192, 64q/8kv heads of 128, f 28672) at one
+    # layer; a 4096-token vocabulary keeps the host oracle's embedding small
+    cfg = llama_tiny_config(n_layers=1, n_heads=64, n_kv_heads=8, head_dim=128, ffn_dim=28672,
+                            vocab_size=4096, max_seq=256)
+    return init_weights_llama(cfg, seed=5)
+
+
+@pytest.mark.parametrize("mode", [ParallelMode.SP, ParallelMode.TP])
+def test_70b_width_prefill_and_decode_vs_oracle(w70b_l1, mode):
+    """configs[3] model width: prefill (span logits) and a decode step at P=2
+    against the fp32 oracle on the same bf16 weights."""
+    rng = np.random.default_rng(4)
+    prompt = [int(t) for t in rng.integers(0, 4096, size=24)]
+    eng = Engine(device_weights(w70b_l1, 2), LoopbackGroup(2), ShiftPolicy.fixed_tp())
+    s = eng.new_sequence(0, capacity=48)
+    lg, _ = eng.step(Batch(BatchKind.PREFILL, [BatchItem(s, prompt)]), mode=mode,
+                     span_logits=True)
+    want, _ = oracle.forward_reference(w70b_l1, prompt)
+    assert rel_err(lg[0].cpu().numpy(), want) <= LOGIT_TOL
+    tok = int(np.argmax(want[-1]))
+    lg, _ = eng.step(Batch(BatchKind.DECODE, [BatchItem(s, [tok])]), mode=mode)
+    want2, _ = oracle.forward_reference(w70b_l1, prompt + [tok])
     assert rel_err(lg[0].cpu().numpy(), want2[-1]) <= LOGIT_TOL
 
 
