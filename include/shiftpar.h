@@ -99,6 +99,11 @@ sp_status sp_gemm_bf16_qkv_rope(const void* A, int64_t lda, const void* B, int64
                                 const float* rope_table, void* q_out, int64_t ldq, void* k_pool,
                                 void* v_pool, int q_heads, int kv_heads, int block_size,
                                 void* stream);
+/* Kernel sp_gemm_bf16 runs for a shape on a GPU with `sms` SMs (host only,
+ * split-K workspace assumed): 0 = swap-AB decode kernel, 1 = 2-CTA 256x256
+ * pairs, 256/128/64/32 = 1-CTA 128xBN tiles (wave-model choice); -1 = bad
+ * arguments.  For diagnostics and tests. */
+int sp_gemm_plan(int M, int N, int K, int epilogue, int sms);
 /* Number of f32 [M][N] partial slabs SP_EPI_PARTIAL_F32 writes for this shape
  * (1 outside the split-K regime).  Host-only, deterministic. */
 int sp_gemm_partials(int M, int N, int K);

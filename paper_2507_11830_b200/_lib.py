@@ -41,6 +41,7 @@ SIGNATURES = {
     "sp_add_rmsnorm": (_c_int, [_vp, _i64, _vp, _c_int, _vp, _f32, _vp, _vp, _i64, _c_int, _c_int,
                                 _vp]),
     "sp_gemm_partials": (_c_int, [_c_int, _c_int, _c_int]),
+    "sp_gemm_plan": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int]),
     "sp_ipc_export": (_c_int, [_vp, _vp, ctypes.POINTER(_i64)]),
     "sp_attention_prefill_split": (_c_int, [_vp, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp,
                                             _vp, _vp, _vp, _c_int, _vp, _c_int, _vp, _i64, _c_int,

@@ -1384,6 +1384,56 @@ extern "C" int sp_gemm_partials(int M, int N, int K) {
   return (int)swap_splits<256>(N, K, sms);
 }
 
+// Tile of the non-decode regime: 256 (2-CTA pairs unless *no_pair) or a
+// narrower 1-CTA width.
+static int plan_tile(int M, int N, int epilogue, int sms, bool* no_pair) {
+  using namespace sp::gemm;
+  const int64_t m_tiles = cdiv(M, BM);
+  int bn = 256;
+  *no_pair = false;
+  if (m_tiles * cdiv(N, 256) < sms && epilogue != SP_EPI_SWIGLU) {
+    // fewer 128x256 tiles than SMs: pick the tile by a wave model — cost =
+    // waves x per-SM tile work (relative to half a 256x256 pair tile) x the
+    // measured per-SM efficiency loss of 1-CTA tiles vs 2-CTA pairs
+    // (tools/gemm_sweep.py: ~1.3 for 128x256, ~1.4 for 128x128, ~1.7 for 128x64,
+    // ~2.5 for 128x32).  All candidates share the K loop: bit-identical.
+    const bool pair_ok = M >= 256 && N % 256 == 0;
+    double best = pair_ok ? (double)cdiv(cdiv(M, 256) * cdiv(N, 256), sms / 2) : 1e30;
+    bn = 256;
+    bool use_pair = pair_ok;
+    const struct { int bn; double f; } cands[] = {{256, 1.3}, {128, 1.4}, {64, 1.7}, {32, 2.5}};
+    for (const auto& c : cands) {
+      const double cost = (double)cdiv(m_tiles * cdiv(N, c.bn), sms) * (c.bn / 256.0) * c.f;
+      if (cost < best) {
+        best = cost;
+        bn = c.bn;
+        use_pair = false;
+      }
+    }
+    *no_pair = !use_pair;
+  }
+  return bn;
+}
+
+// Which kernel sp_gemm_bf16 runs for this shape on `sms` SMs (host only; a
+// split-K workspace assumed): 0 = swap-AB decode kernel, 1 = 2-CTA 256x256
+// pairs, 256/128/64/32 = 1-CTA 128xBN tiles.  Diagnostics and tests.
+extern "C" int sp_gemm_plan(int M, int N, int K, int epilogue, int sms) {
+  (void)K;
+  if (M <= 0 || N <= 0 || sms <= 0) return -1;
+  if (swap_regime(M, N, sms)) return 0;
+  bool no_pair = false;
+  const int bn = plan_tile(M, N, epilogue, sms, &no_pair);
+  if (const char* f = getenv("SP_GEMM_FORCE_BN")) {
+    const int fb = atoi(f);
+    if ((fb == 32 || fb == 64 || fb == 128 || fb == 256) && epilogue != SP_EPI_SWIGLU)
+      return fb == 256 && M >= 256 && N % 256 == 0 ? 1 : fb;
+  }
+  const char* e = getenv("SP_GEMM_2CTA");
+  if (bn == 256 && M >= 256 && N % 256 == 0 && !no_pair && !(e && e[0] == '0')) return 1;
+  return bn;
+}
+
 extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
                                   int64_t a_chunk_stride, const void* B, int64_t ldb, void* D,
                                   int64_t ldd, int M, int N, int K, int epilogue,
@@ -1417,7 +1467,6 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
   //  * otherwise                                     -> narrower N tiles (128/64/32),
   //    bit-identical to BN=256 (same K loop)
   const int sms = sm_count();
-  const int64_t m_tiles = cdiv(M, BM);
   int bn = 256;
   bool no_pair = false;
   if (swap_regime(M, N, sms)) {
@@ -1436,27 +1485,7 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
                             peer_width, peer_stride, stream, g_ws, g_ws_bytes);
     if (rc >= 0) return rc;
   }
-  if (m_tiles * cdiv(N, 256) < sms && epilogue != SP_EPI_SWIGLU) {
-    // fewer 128x256 tiles than SMs: pick the tile by a wave model — cost =
-    // waves x per-SM tile work (relative to half a 256x256 pair tile) x the
-    // measured per-SM efficiency loss of 1-CTA tiles vs 2-CTA pairs
-    // (tools/gemm_sweep.py: ~1.3 for 128x256, ~1.4 for 128x128, ~1.7 for 128x64,
-    // ~2.5 for 128x32).  All candidates share the K loop: bit-identical.
-    const bool pair_ok = M >= 256 && N % 256 == 0;
-    double best = pair_ok ? (double)cdiv(cdiv(M, 256) * cdiv(N, 256), sms / 2) : 1e30;
-    bn = 256;
-    bool use_pair = pair_ok;
-    const struct { int bn; double f; } cands[] = {{256, 1.3}, {128, 1.4}, {64, 1.7}, {32, 2.5}};
-    for (const auto& c : cands) {
-      const double cost = (double)cdiv(m_tiles * cdiv(N, c.bn), sms) * (c.bn / 256.0) * c.f;
-      if (cost < best) {
-        best = cost;
-        bn = c.bn;
-        use_pair = false;
-      }
-    }
-    no_pair = !use_pair;
-  }
+  bn = plan_tile(M, N, epilogue, sms, &no_pair);
   if (epilogue == SP_EPI_PARTIAL_F32) epilogue = SP_EPI_STORE_F32;  // one "partial" = the result
   if (const char* f = getenv("SP_GEMM_FORCE_BN")) {
     const int fb = atoi(f);

@@ -259,3 +259,18 @@ def test_attention_split_plan_covers_every_key_tile_once():
     # a pass that already fills the GPU, or a workspace too small: no plan
     assert attention_split_plan(wl, [T], [0], tt, hk=8, sms=148, max_slots=4096) is None
     assert attention_split_plan(wl, [T], [0], tt, hk=1, sms=148, max_slots=1) is None
+
+
+@pytest.mark.parametrize("M,N,epi,want", [
+    (1, 4096, 1, 0), (64, 4096, 5, 0), (256, 4096, 2, 0),    # decode: swap-AB (M <= 256)
+    (1024, 4096, 2, 1), (8192, 6144, 0, 1),                   # prefill: 2-CTA pairs
+    (512, 4096, 2, 128), (512, 6144, 0, 1),                   # wave model at small per-rank M
+    (300, 28672, 3, 1), (1, 128256, 1, 256)])                 # SwiGLU forces 256; LM head row
+def test_gemm_plan_regimes(M, N, epi, want, monkeypatch):
+    """The host-side GEMM plan (sp_gemm_plan, the same function sp_gemm_bf16
+    dispatches on) picks the documented regime per shape on 148 SMs."""
+    for k in ("SP_GEMM_NO_SPLITK", "SP_GEMM_FORCE_BN", "SP_GEMM_2CTA"):
+        monkeypatch.delenv(k, raising=False)
+    assert _lib.load().sp_gemm_plan(M, N, 4096, epi, 148) == want
+    monkeypatch.setenv("SP_GEMM_NO_SPLITK", "1")  # tests pin the non-decode regime this way
+    assert _lib.load().sp_gemm_plan(M, N, 4096, epi, 148) != 0
