@@ -42,6 +42,12 @@ typedef int sp_status;
                                 n = sp_gemm_partials(M, N, K); the consumer sums them in
                                 ascending order (sp_add_rmsnorm n_add) — the split-K
                                 reduction fused into the next kernel */
+/* Flag OR-ed into `epilogue`: ordered regime — every D element is ONE
+ * ascending-K chain of 16-deep MMA steps (never the split-K decode regime),
+ * so column/row splits of an operand recombine bit-exactly at any M
+ * (the matmul contract of tensor_core.py:1-28; used by the operator-level
+ * drop-in paper_2507_11830_b200.tensor_core). */
+#define SP_GEMM_ORDERED 0x100
 
 /* -------------------------------------------------------------- runtime */
 const char* sp_last_error(void);
@@ -236,6 +242,17 @@ sp_status sp_peer_allreduce_add_rmsnorm(const unsigned long long* part_ptrs, int
                                         float* x, int64_t ldx, const float* gain, float eps,
                                         void* out_bf16, int64_t ldo, int rows, int hidden,
                                         void* stream);
+/* Two-shot variant for prefill-size passes (TP all-reduce, fabric.py:117-143,
+ * at parallel_engine.py:371/379 followed by the next rms_norm): rank my_rank
+ * owns rows [lo, hi) of the contiguous split of `rows` (remainder to low
+ * ranks); for each it sums the P f32 partials part_ptrs[s] ([rows][hidden],
+ * ascending s), adds them into its residual row x, and stores bf16(gain * x /
+ * sqrt(mean(x^2) + eps)) into EVERY rank's xn_ptrs[s] row (row stride ldo).
+ * Bit-identical to the one-shot kernel per row; reads (P-1)/P of the bytes. */
+sp_status sp_peer_reduce_scatter_rmsnorm(const unsigned long long* part_ptrs, int peers,
+                                         int my_rank, float* x, int64_t ldx, const float* gain,
+                                         float eps, const unsigned long long* xn_ptrs,
+                                         int64_t ldo, int rows, int hidden, void* stream);
 
 /* ---------------------------------------------- reductions and heads
  * In-process (loopback) all-reduce: dst = a + b, f32, ascending order as in
@@ -249,12 +266,32 @@ sp_status sp_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out);
 sp_status sp_ipc_import(const void* handle, int64_t offset, void** ptr_out);
 
 sp_status sp_add_f32(const float* a, const float* b, float* dst, int64_t n, void* stream);
+/* f64 variant for callers that hand the reference-shaped DeviceGroup f64
+ * shards (paper_2507_11830_b200.collectives, fabric.py:117-143). */
+sp_status sp_add_f64(const double* a, const double* b, double* dst, int64_t n, void* stream);
+
+/* ------------------------------------- operator-level drop-in primitives
+ * The reference's primitive API beyond matmul/attend_cached, f32 in and out
+ * (paper_2507_11830_b200.tensor_core binds them):
+ *   sp_rms_norm_f32      rms_norm(x, gain, eps)   tensor_core.py:115-123
+ *                        out = gain * (x / sqrt(mean(x^2) + eps)) per row
+ *   sp_gelu_f32          gelu(x)                  tensor_core.py:126-132 (tanh form)
+ *   sp_softmax_rows_f32  softmax_rows(x)          tensor_core.py:105-112
+ *                        shift by row max; -inf entries give 0 */
+sp_status sp_rms_norm_f32(const float* x, int64_t ldx, const float* gain, float eps, float* out,
+                          int64_t ldo, int rows, int hidden, void* stream);
+sp_status sp_gelu_f32(const float* x, float* out, int64_t n, void* stream);
+sp_status sp_softmax_rows_f32(const float* x, int64_t ldx, float* out, int64_t ldo, int rows,
+                              int width, void* stream);
 /* greedy_token (model.py:303-307): per row argmax, lowest index wins ties. */
 sp_status sp_argmax(const float* logits, int64_t ld, int rows, int vocab, int32_t* idx,
                     float* val, void* stream);
 /* dst[r, :] = src[idx[r], :] for f32 rows (end-row / tail selection). */
 sp_status sp_gather_rows_f32(const float* src, int64_t lds, const int32_t* idx, float* dst,
                              int64_t ldd, int rows, int width, void* stream);
+/* The same for bf16 rows (end rows of a pushed final-norm buffer). */
+sp_status sp_gather_rows_bf16(const void* src, int64_t lds, const int32_t* idx, void* dst,
+                              int64_t ldd, int rows, int width, void* stream);
 
 #ifdef __cplusplus
 }

@@ -25,9 +25,12 @@ from .engine import (  # noqa: F401
 )
 from .errors import CacheOverflow, ConfigError, ContractViolation, LibraryMissing  # noqa: F401
 from .fabric import DeviceGroup, LoopbackGroup, NcclGroup  # noqa: F401
-from .flops import FlopMeter, PassShape, flop_count, shard_bounds, shard_rows  # noqa: F401
+from .flops import (FlopMeter, PassShape, flop_count, shard_bounds, shard_rows,  # noqa: F401
+                    swiftkv_flop_ratio)
 from .kv_cache import AXIS_ORDER, BlockAllocator, KvCache, KvPool, LayoutFingerprint  # noqa: F401
-from .weights import ModelWeights  # noqa: F401
+from .weights import (ModelWeights, TpShard, check_shard_containment, memory_report,  # noqa: F401
+                      tp_shard_view)
+from . import collectives, tensor_core  # noqa: F401,E402
 from . import spec_decode  # noqa: F401,E402
 
 __version__ = "0.1.0"

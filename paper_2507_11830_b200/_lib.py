@@ -37,6 +37,8 @@ SIGNATURES = {
     "sp_peer_allreduce_add_rmsnorm": (_c_int, [_vp, _c_int, _c_int, _vp, _i64, _vp, _f32, _vp, _i64,
                                                _c_int,
                                                _c_int, _vp]),
+    "sp_peer_reduce_scatter_rmsnorm": (_c_int, [_vp, _c_int, _c_int, _vp, _i64, _vp, _f32, _vp,
+                                                _i64, _c_int, _c_int, _vp]),
     "sp_embed": (_c_int, [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _vp]),
     "sp_add_rmsnorm": (_c_int, [_vp, _i64, _vp, _c_int, _vp, _f32, _vp, _vp, _i64, _c_int, _c_int,
                                 _vp]),
@@ -63,6 +65,11 @@ SIGNATURES = {
     "sp_add_f32": (_c_int, [_vp, _vp, _vp, _i64, _vp]),
     "sp_argmax": (_c_int, [_vp, _i64, _c_int, _c_int, _vp, _vp, _vp]),
     "sp_gather_rows_f32": (_c_int, [_vp, _i64, _vp, _vp, _i64, _c_int, _c_int, _vp]),
+    "sp_gather_rows_bf16": (_c_int, [_vp, _i64, _vp, _vp, _i64, _c_int, _c_int, _vp]),
+    "sp_rms_norm_f32": (_c_int, [_vp, _i64, _vp, _f32, _vp, _i64, _c_int, _c_int, _vp]),
+    "sp_gelu_f32": (_c_int, [_vp, _vp, _i64, _vp]),
+    "sp_add_f64": (_c_int, [_vp, _vp, _vp, _i64, _vp]),
+    "sp_softmax_rows_f32": (_c_int, [_vp, _i64, _vp, _i64, _c_int, _c_int, _vp]),
 }
 
 _lib = None

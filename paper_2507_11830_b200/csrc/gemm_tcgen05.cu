@@ -1360,17 +1360,33 @@ static int launch_pair(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   return check_launch("gemm_pair_kernel");
 }
 
-// split-K workspace (set once by the host; never allocated in the hot path)
-static float* g_ws = nullptr;
-static int64_t g_ws_bytes = 0;
+// split-K workspace per device (registered by the host, never allocated in
+// the hot path; the host keeps every registered buffer alive because captured
+// CUDA graphs hold its address)
+static constexpr int kMaxDevices = 64;
+static float* g_ws[kMaxDevices] = {};
+static int64_t g_ws_bytes[kMaxDevices] = {};
 
+static int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 || d >= kMaxDevices ? 0 : d;
+}
 
 extern "C" sp_status sp_gemm_set_workspace(void* ws, int64_t bytes) {
   if (bytes < 0 || (ws == nullptr && bytes > 0)) return fail(kInvalid, "gemm workspace: bad args");
   if (reinterpret_cast<uintptr_t>(ws) & 15) return fail(kInvalid, "gemm workspace must be 16B aligned");
-  g_ws = static_cast<float*>(ws);
-  g_ws_bytes = bytes;
+  const int d = cur_device();
+  g_ws[d] = static_cast<float*>(ws);
+  g_ws_bytes[d] = bytes;
   return kOk;
+}
+
+static int64_t swap_splits_for(int M, int N, int K, int sms) {
+  if (M <= 32) return swap_splits<32>(N, K, sms);
+  if (M <= 64) return swap_splits<64>(N, K, sms);
+  if (M <= 128) return swap_splits<128>(N, K, sms);
+  return swap_splits<256>(N, K, sms);
 }
 
 extern "C" int sp_gemm_partials(int M, int N, int K) {
@@ -1378,10 +1394,7 @@ extern "C" int sp_gemm_partials(int M, int N, int K) {
   if (M <= 0 || N <= 0 || K <= 0) return 1;
   const int sms = sm_count();
   if (!swap_regime(M, N, sms)) return 1;
-  if (M <= 32) return (int)swap_splits<32>(N, K, sms);
-  if (M <= 64) return (int)swap_splits<64>(N, K, sms);
-  if (M <= 128) return (int)swap_splits<128>(N, K, sms);
-  return (int)swap_splits<256>(N, K, sms);
+  return (int)swap_splits_for(M, N, K, sms);
 }
 
 // Tile of the non-decode regime: 256 (2-CTA pairs unless *no_pair) or a
@@ -1415,23 +1428,39 @@ static int plan_tile(int M, int N, int epilogue, int sms, bool* no_pair) {
   return bn;
 }
 
-// Which kernel sp_gemm_bf16 runs for this shape on `sms` SMs (host only; a
-// split-K workspace assumed): 0 = swap-AB decode kernel, 1 = 2-CTA 256x256
-// pairs, 256/128/64/32 = 1-CTA 128xBN tiles.  Diagnostics and tests.
-extern "C" int sp_gemm_plan(int M, int N, int K, int epilogue, int sms) {
-  (void)K;
-  if (M <= 0 || N <= 0 || sms <= 0) return -1;
-  if (swap_regime(M, N, sms)) return 0;
+// THE dispatch decision of sp_gemm_bf16 (and what sp_gemm_plan reports):
+// 0 = swap-AB decode kernel, 1 = 2-CTA 256x256 pairs, 256/128/64/32 = 1-CTA
+// 128xBN tiles.  Env overrides apply in one order: SP_GEMM_NO_SPLITK (inside
+// swap_regime), SP_GEMM_FORCE_BN, SP_GEMM_2CTA.  The swap-AB regime needs the
+// device's split-K workspace when it splits K (except for raw partials).
+static int gemm_plan(int M, int N, int K, int epilogue, int sms, const float* ws,
+                     int64_t ws_bytes, bool ordered = false) {
+  if (!ordered && swap_regime(M, N, sms)) {
+    const int64_t ks = swap_splits_for(M, N, K, sms);
+    if (ks == 1 || epilogue == SP_EPI_PARTIAL_F32 ||
+        (ws && ks * (int64_t)M * N * 4 <= ws_bytes))
+      return 0;
+  }
+  if (epilogue == SP_EPI_PARTIAL_F32) epilogue = SP_EPI_STORE_F32;
   bool no_pair = false;
-  const int bn = plan_tile(M, N, epilogue, sms, &no_pair);
+  int bn = plan_tile(M, N, epilogue, sms, &no_pair);
   if (const char* f = getenv("SP_GEMM_FORCE_BN")) {
     const int fb = atoi(f);
-    if ((fb == 32 || fb == 64 || fb == 128 || fb == 256) && epilogue != SP_EPI_SWIGLU)
-      return fb == 256 && M >= 256 && N % 256 == 0 ? 1 : fb;
+    if ((fb == 32 || fb == 64 || fb == 128 || fb == 256) && epilogue != SP_EPI_SWIGLU) {
+      bn = fb;
+      no_pair = false;
+    }
   }
   const char* e = getenv("SP_GEMM_2CTA");
   if (bn == 256 && M >= 256 && N % 256 == 0 && !no_pair && !(e && e[0] == '0')) return 1;
   return bn;
+}
+
+extern "C" int sp_gemm_plan(int M, int N, int K, int epilogue, int sms) {
+  if (M <= 0 || N <= 0 || K <= 0 || sms <= 0) return -1;
+  const int d = cur_device();
+  return gemm_plan(M, N, K, epilogue & ~SP_GEMM_ORDERED, sms, g_ws[d], g_ws_bytes[d],
+                   (epilogue & SP_GEMM_ORDERED) != 0);
 }
 
 extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
@@ -1439,6 +1468,8 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
                                   int64_t ldd, int M, int N, int K, int epilogue,
                                   int64_t peer_width, int64_t peer_stride, void* stream) {
   using namespace sp::gemm;
+  const bool ordered = (epilogue & SP_GEMM_ORDERED) != 0;
+  epilogue &= ~SP_GEMM_ORDERED;
   if (M < 0 || N <= 0 || K <= 0) return fail(kInvalid, "gemm: bad M/N/K");
   if (M == 0) return kOk;
   if (!A || !B || !D) return fail(kInvalid, "gemm: null pointer");
@@ -1467,40 +1498,28 @@ extern "C" sp_status sp_gemm_bf16(const void* A, int64_t lda, int64_t a_kchunk,
   //  * otherwise                                     -> narrower N tiles (128/64/32),
   //    bit-identical to BN=256 (same K loop)
   const int sms = sm_count();
-  int bn = 256;
-  bool no_pair = false;
-  if (swap_regime(M, N, sms)) {
-    int rc = -1;
+  const int dev = cur_device();
+  const int plan = gemm_plan(M, N, K, epilogue, sms, g_ws[dev], g_ws_bytes[dev], ordered);
+  if (plan == 0) {
+    float* ws = g_ws[dev];
+    const int64_t wsb = g_ws_bytes[dev];
     if (M <= 32)
-      rc = launch_swap<32>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
-                           peer_width, peer_stride, stream, g_ws, g_ws_bytes);
-    else if (M <= 64)
-      rc = launch_swap<64>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
-                           peer_width, peer_stride, stream, g_ws, g_ws_bytes);
-    else if (M <= 128)
-      rc = launch_swap<128>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
-                            peer_width, peer_stride, stream, g_ws, g_ws_bytes);
-    else
-      rc = launch_swap<256>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
-                            peer_width, peer_stride, stream, g_ws, g_ws_bytes);
-    if (rc >= 0) return rc;
+      return launch_swap<32>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
+                             peer_width, peer_stride, stream, ws, wsb);
+    if (M <= 64)
+      return launch_swap<64>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
+                             peer_width, peer_stride, stream, ws, wsb);
+    if (M <= 128)
+      return launch_swap<128>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
+                              peer_width, peer_stride, stream, ws, wsb);
+    return launch_swap<256>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
+                            peer_width, peer_stride, stream, ws, wsb);
   }
-  bn = plan_tile(M, N, epilogue, sms, &no_pair);
   if (epilogue == SP_EPI_PARTIAL_F32) epilogue = SP_EPI_STORE_F32;  // one "partial" = the result
-  if (const char* f = getenv("SP_GEMM_FORCE_BN")) {
-    const int fb = atoi(f);
-    if ((fb == 32 || fb == 64 || fb == 128 || fb == 256) && epilogue != SP_EPI_SWIGLU) {
-      bn = fb;
-      no_pair = false;
-    }
-  }
-  if (bn == 256 && M >= 256 && N % 256 == 0 && !no_pair) {
-    const char* e = getenv("SP_GEMM_2CTA");
-    if (!(e && e[0] == '0'))
-      return launch_pair(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
-                         peer_width, peer_stride, stream);
-  }
-  switch (bn) {
+  if (plan == 1)
+    return launch_pair(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue,
+                       peer_width, peer_stride, stream);
+  switch (plan) {
     case 256: return launch<256>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue, peer_width, peer_stride, stream);
     case 128: return launch<128>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue, peer_width, peer_stride, stream);
     case 64: return launch<64>(A, lda, a_kchunk, a_chunk_stride, B, ldb, D, ldd, M, N, K, epilogue, peer_width, peer_stride, stream);

@@ -143,9 +143,103 @@ __global__ void peer_allreduce_norm_kernel(const unsigned long long* __restrict_
   }
 }
 
+// Two-shot TP all-reduce for prefill-size passes (reduce-scatter + all-gather
+// over the same peer buffers): rank r owns rows [lo, hi) of the contiguous
+// split (remainder to low ranks, flops.py:68-80); for each owned row it sums
+// the P partials in ascending rank order (exactly the one-shot sum), adds them
+// into its residual row, normalises, and PUSHES the bf16 normed row into every
+// rank's xn buffer (NVLink stores).  Per rank: reads (P-1)/P*M*h*4 bytes of
+// peer partials and writes (P-1)/P*M*h*2, vs (P-1)*M*h*4 reads one-shot.  The
+// residual stays row-sharded between reductions (only the owner reads a row
+// again), so no f32 all-gather is needed; the final reduction pushes the
+// final-normed rows the LM head needs.
+template <int VEC>
+__global__ void peer_reduce_scatter_norm_kernel(const unsigned long long* __restrict__ part_ptrs,
+                                                int peers, int row_lo, float* __restrict__ x,
+                                                int64_t ldx, const float* __restrict__ gain,
+                                                float eps,
+                                                const unsigned long long* __restrict__ xn_ptrs,
+                                                int64_t ldo, int hidden) {
+  pdl_wait();
+  pdl_trigger();
+  const int r = row_lo + blockIdx.x;
+  float* xr = x + (int64_t)r * ldx;
+  float v[VEC * 4];
+  float ssq[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = (i * blockDim.x + threadIdx.x) * 4;
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c < hidden) {
+      float4 sum = *reinterpret_cast<const float4*>(
+          reinterpret_cast<const float*>(part_ptrs[0]) + (int64_t)r * hidden + c);
+      for (int s = 1; s < peers; ++s) {
+        const float4 q = *reinterpret_cast<const float4*>(
+            reinterpret_cast<const float*>(part_ptrs[s]) + (int64_t)r * hidden + c);
+        sum.x += q.x;
+        sum.y += q.y;
+        sum.z += q.z;
+        sum.w += q.w;
+      }
+      t = *reinterpret_cast<const float4*>(xr + c);
+      t.x += sum.x;
+      t.y += sum.y;
+      t.z += sum.z;
+      t.w += sum.w;
+      *reinterpret_cast<float4*>(xr + c) = t;
+    }
+    v[4 * i + 0] = t.x;
+    v[4 * i + 1] = t.y;
+    v[4 * i + 2] = t.z;
+    v[4 * i + 3] = t.w;
+    ssq[i] = ((t.x * t.x + t.y * t.y) + t.z * t.z) + t.w * t.w;
+  }
+  __shared__ float red[256];
+  const float den = sqrtf(rms_chunk_sum<VEC>(ssq, hidden, red) / (float)hidden + eps);
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = (i * blockDim.x + threadIdx.x) * 4;
+    if (c < hidden) {
+      const float4 g = *reinterpret_cast<const float4*>(gain + c);
+      uint2 u;
+      u.x = pack_bf16x2(g.x * (v[4 * i + 0] / den), g.y * (v[4 * i + 1] / den));
+      u.y = pack_bf16x2(g.z * (v[4 * i + 2] / den), g.w * (v[4 * i + 3] / den));
+      for (int s = 0; s < peers; ++s)
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(xn_ptrs[s]) +
+                                  (int64_t)r * ldo + c) = u;
+    }
+  }
+}
+
 }  // namespace sp
 
 using namespace sp;
+
+extern "C" sp_status sp_peer_reduce_scatter_rmsnorm(const unsigned long long* part_ptrs, int peers,
+                                                    int my_rank, float* x, int64_t ldx,
+                                                    const float* gain, float eps,
+                                                    const unsigned long long* xn_ptrs,
+                                                    int64_t ldo, int rows, int hidden,
+                                                    void* stream) {
+  if (!part_ptrs || !xn_ptrs || !gain || peers < 1 || my_rank < 0 || my_rank >= peers ||
+      rows < 0 || hidden <= 0 || hidden % 4 || ldx % 4 || ldo % 4)
+    return fail(kInvalid, "peer_reduce_scatter_rmsnorm: bad arguments");
+  const int base = rows / peers, rem = rows % peers;
+  const int lo = my_rank * base + (my_rank < rem ? my_rank : rem);
+  const int mine = base + (my_rank < rem ? 1 : 0);
+  if (mine == 0) return kOk;
+  const int threads = norm_block_threads(mine, hidden);
+  const int per = (hidden + threads * 4 - 1) / (threads * 4);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  switch (per) {
+    case 1: launch_k(peer_reduce_scatter_norm_kernel<1>, mine, threads, 0, st, part_ptrs, peers, lo, x, ldx, gain, eps, xn_ptrs, ldo, hidden); break;
+    case 2: launch_k(peer_reduce_scatter_norm_kernel<2>, mine, threads, 0, st, part_ptrs, peers, lo, x, ldx, gain, eps, xn_ptrs, ldo, hidden); break;
+    case 3: case 4: launch_k(peer_reduce_scatter_norm_kernel<4>, mine, threads, 0, st, part_ptrs, peers, lo, x, ldx, gain, eps, xn_ptrs, ldo, hidden); break;
+    case 5: case 6: case 7: case 8: launch_k(peer_reduce_scatter_norm_kernel<8>, mine, threads, 0, st, part_ptrs, peers, lo, x, ldx, gain, eps, xn_ptrs, ldo, hidden); break;
+    default: return fail(kUnsupported, "peer_reduce_scatter_rmsnorm: hidden > 8192");
+  }
+  return check_launch("peer_reduce_scatter_norm_kernel");
+}
 
 extern "C" sp_status sp_peer_allreduce_add_rmsnorm(const unsigned long long* part_ptrs, int peers,
                                                    int slabs, float* x, int64_t ldx,

@@ -500,3 +500,141 @@ extern "C" sp_status sp_gather_rows_f32(const float* src, int64_t lds, const int
   launch_k(gather_rows_kernel, rows, 256, 0, S(stream), src, lds, idx, dst, ldd, width);
   return check_launch("gather_rows_kernel");
 }
+
+// ------------------------------------------ operator-level drop-in kernels
+// The reference's primitive API (tensor_core.py:105-132) as device kernels for
+// paper_2507_11830_b200.tensor_core: f32 in, f32 out, one row per block.
+__global__ void rms_norm_f32_kernel(const float* __restrict__ x, int64_t ldx,
+                                    const float* __restrict__ gain, float eps,
+                                    float* __restrict__ out, int64_t ldo, int hidden) {
+  __shared__ float red[32];
+  pdl_wait();
+  pdl_trigger();
+  const float* row = x + (int64_t)blockIdx.x * ldx;
+  float s = 0.f;
+  for (int c = threadIdx.x; c < hidden; c += blockDim.x) s += row[c] * row[c];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float den = sqrtf(red[0] / (float)hidden + eps);  // gain * (x / sqrt(mean + eps))
+  float* o = out + (int64_t)blockIdx.x * ldo;
+  for (int c = threadIdx.x; c < hidden; c += blockDim.x) o[c] = gain[c] * (row[c] / den);
+}
+
+__global__ void gelu_f32_kernel(const float* __restrict__ x, float* __restrict__ out, int64_t n) {
+  const float c = 0.7978845608028654f, k = 0.044715f;  // sqrt(2/pi), tanh-form GeLU
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[i];
+    out[i] = 0.5f * v * (1.f + tanhf(c * (v + k * v * v * v)));
+  }
+}
+
+__global__ void softmax_rows_f32_kernel(const float* __restrict__ x, int64_t ldx,
+                                        float* __restrict__ out, int64_t ldo, int width) {
+  __shared__ float red[32];
+  pdl_wait();
+  pdl_trigger();
+  const float* row = x + (int64_t)blockIdx.x * ldx;
+  float* o = out + (int64_t)blockIdx.x * ldo;
+  const int w = blockDim.x >> 5, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float m = -INFINITY;
+  for (int c = threadIdx.x; c < width; c += blockDim.x) m = fmaxf(m, row[c]);
+#pragma unroll
+  for (int s = 16; s; s >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, s));
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  m = -INFINITY;
+  for (int i = 0; i < w; ++i) m = fmaxf(m, red[i]);
+  __syncthreads();
+  float sum = 0.f;
+  for (int c = threadIdx.x; c < width; c += blockDim.x) {
+    const float e = expf(row[c] - m);  // -inf entries (masked keys) -> 0
+    o[c] = e;
+    sum += e;
+  }
+#pragma unroll
+  for (int s = 16; s; s >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, s);
+  if (lane == 0) red[warp] = sum;
+  __syncthreads();
+  sum = 0.f;
+  for (int i = 0; i < w; ++i) sum += red[i];
+  for (int c = threadIdx.x; c < width; c += blockDim.x) o[c] = o[c] / sum;
+}
+
+extern "C" sp_status sp_rms_norm_f32(const float* x, int64_t ldx, const float* gain, float eps,
+                                     float* out, int64_t ldo, int rows, int hidden, void* stream) {
+  if (rows < 0 || hidden <= 0 || ldx < hidden || ldo < hidden)
+    return fail(kInvalid, "rms_norm_f32: bad shape");
+  if (rows == 0) return kOk;
+  if (!x || !gain || !out) return fail(kInvalid, "rms_norm_f32: null pointer");
+  launch_k(rms_norm_f32_kernel, rows, 256, 0, S(stream), x, ldx, gain, eps, out, ldo, hidden);
+  return check_launch("rms_norm_f32_kernel");
+}
+
+extern "C" sp_status sp_gelu_f32(const float* x, float* out, int64_t n, void* stream) {
+  if (n < 0) return fail(kInvalid, "gelu_f32: n < 0");
+  if (n == 0) return kOk;
+  if (!x || !out) return fail(kInvalid, "gelu_f32: null pointer");
+  launch_k(gelu_f32_kernel, grid_for(n, 256), 256, 0, S(stream), x, out, n);
+  return check_launch("gelu_f32_kernel");
+}
+
+extern "C" sp_status sp_softmax_rows_f32(const float* x, int64_t ldx, float* out, int64_t ldo,
+                                         int rows, int width, void* stream) {
+  if (rows < 0 || width <= 0 || ldx < width || ldo < width)
+    return fail(kInvalid, "softmax_rows_f32: bad shape");
+  if (rows == 0) return kOk;
+  if (!x || !out) return fail(kInvalid, "softmax_rows_f32: null pointer");
+  launch_k(softmax_rows_f32_kernel, rows, 256, 0, S(stream), x, ldx, out, ldo, width);
+  return check_launch("softmax_rows_f32_kernel");
+}
+
+__global__ void add_f64_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                               double* __restrict__ d, int64_t n) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = a[i] + b[i];
+}
+
+extern "C" sp_status sp_add_f64(const double* a, const double* b, double* dst, int64_t n,
+                                void* stream) {
+  if (n < 0) return fail(kInvalid, "add_f64: n < 0");
+  if (n == 0) return kOk;
+  if (!a || !b || !dst) return fail(kInvalid, "add_f64: null pointer");
+  launch_k(add_f64_kernel, grid_for(n, 256), 256, 0, S(stream), a, b, dst, n);
+  return check_launch("add_f64_kernel");
+}
+
+__global__ void gather_rows_u16_kernel(const uint16_t* __restrict__ src, int64_t lds,
+                                       const int32_t* __restrict__ idx, uint16_t* __restrict__ dst,
+                                       int64_t ldd, int width) {
+  pdl_wait();
+  pdl_trigger();
+  const uint16_t* s = src + (int64_t)idx[blockIdx.x] * lds;
+  uint16_t* d = dst + (int64_t)blockIdx.x * ldd;
+  for (int c = threadIdx.x; c < width; c += blockDim.x) d[c] = s[c];
+}
+
+extern "C" sp_status sp_gather_rows_bf16(const void* src, int64_t lds, const int32_t* idx,
+                                         void* dst, int64_t ldd, int rows, int width,
+                                         void* stream) {
+  if (rows < 0 || width <= 0) return fail(kInvalid, "gather_rows_bf16: bad shape");
+  if (rows == 0) return kOk;
+  launch_k(gather_rows_u16_kernel, rows, 256, 0, S(stream), static_cast<const uint16_t*>(src), lds,
+           idx, static_cast<uint16_t*>(dst), ldd, width);
+  return check_launch("gather_rows_u16_kernel");
+}
+

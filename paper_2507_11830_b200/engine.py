@@ -44,7 +44,7 @@ from .errors import CacheOverflow, ConfigError, ContractViolation
 from .fabric import CommRecord, DeviceGroup, LoopbackGroup
 from .flops import FlopMeter, PassShape, flop_count, shard_bounds, shard_rows
 from .kv_cache import KvCache, KvPool
-from .peer import PeerLinks, fused_a2a_enabled
+from .peer import PeerLinks, fused_a2a_enabled, two_shot_min_rows
 from .weights import ModelWeights
 
 
@@ -206,6 +206,7 @@ class _GraphEntry:
         self.kernels = 0
         self.failed = False  # capture raised: this key stays eager
         self.seen = 0  # eager passes run with this key so far
+        self.replays = 0
 
 
 class _RopedQ:
@@ -292,8 +293,9 @@ class Engine:
         self.kv_partition = partition_heads(cfg.kv_heads, self.world_size)
         self.device = weights.embed.device
         ops.device_check()
-        # split-K workspace for decode-size GEMMs (allocated once, never in the hot path)
-        ops.set_gemm_workspace(torch.empty(64 << 20, dtype=torch.uint8, device=self.device))
+        # split-K workspace for decode-size GEMMs: one per device, allocated once and
+        # never freed (captured decode graphs hold its address)
+        ops.ensure_gemm_workspace(self.device)
         if isinstance(group, LoopbackGroup):
             group._add = ops.add_f32
         if self.swiftkv.enabled:
@@ -384,7 +386,8 @@ class Engine:
                 and not getattr(self.group, "_stage", False)  # host-staged collectives
                 and not (mode is ParallelMode.SP and self.sp_degree < self.world_size)
                 and all(len(it.tokens) == 1 for it in batch.items)):
-            graph_key = (mode, len(batch.items), self._bt_width_cap(batch))
+            graph_key = (mode, len(batch.items), self._bt_width_cap(batch),
+                         self._kv_bucket(batch))
         shape = self.pass_shape(batch, span_logits) if graph_key else None
         meta = self._metadata(batch, mode, span_logits, cut, graph_key=graph_key)
         self.group.begin_step(self._step_counter)
@@ -398,6 +401,7 @@ class Engine:
             for kind, per_dev in entry.charges:
                 self.group.charge(kind, per_dev)
             entry.graph.replay()
+            entry.replays += 1
             ops.add_graph_launches(entry.kernels)
             logits = [t.clone() for t in entry.outputs]
             flops = flop_count(shape, mode, self.config, self.world_size)
@@ -433,6 +437,18 @@ class Engine:
         need = max(-(-it.seq.cache.capacity // bs) for it in batch.items)
         w = 1
         while w < need:
+            w *= 2
+        return w
+
+    def _kv_bucket(self, batch: Batch) -> int:
+        """Power-of-two bucket of the longest key window in pages: part of the
+        graph key, so the decode attention's KV split count (chosen from the
+        host max_kv_len at capture and frozen into the graph) follows the
+        context as sequences grow."""
+        bs = self.pool.block_size
+        pages = max(-(-(it.seq.cache.token_count + len(it.tokens)) // bs) for it in batch.items)
+        w = 1
+        while w < pages:
             w *= 2
         return w
 
@@ -716,6 +732,9 @@ class Engine:
 
     # ================================================================= TP
     def _forward_tp(self, meta, batch, meters, span_logits, cut):
+        peer = self._peer
+        if (peer is not None and cut is None and two_shot_min_rows() < meta.M <= peer.max_tokens):
+            return self._forward_tp_two_shot(meta, batch, meters, span_logits, peer)
         cfg, w, g = self.config, self.weights, self.group
         P = self.world_size
         M, h, d = meta.M, cfg.hidden, cfg.head_dim
@@ -833,6 +852,85 @@ class Engine:
             parts[r] = lg
         logits = self._gather_vocab(parts, n_rows)
         return self._split(logits, meta, span_logits and cut is None)
+
+    def _forward_tp_two_shot(self, meta, batch, meters, span_logits, peer):
+        """TP pass for prefill-size M with the two-shot all-reduce over peer
+        memory: each projection's f32 partial goes to the rank's peer buffer,
+        then every rank reduces ITS row slice (ascending rank sum + residual +
+        the next RMSNorm, fused) and pushes the normed bf16 rows into every
+        rank's xn buffer.  The residual x stays row-sharded between reductions
+        (a row is only read again by its owner); the last reduction pushes the
+        final-normed rows for the LM head.  Per rank and all-reduce: reads
+        (P-1)/P*M*h*4 B and writes (P-1)/P*M*h*2 B over NVLink, vs
+        (P-1)*M*h*4 B for the one-shot kernel.  Bit-identical to it and to the
+        collective path (same per-row sums and norm)."""
+        cfg, w, g = self.config, self.weights, self.group
+        P = self.world_size
+        M, h, d = meta.M, cfg.hidden, cfg.head_dim
+        hq, hk = cfg.n_heads // P, cfg.kv_heads // P
+        W, hqw, fl = w.qkv_width, hq * d, cfg.ffn_dim // P
+        dev, eps = self.device, cfg.norm_eps
+        x = torch.empty((M, h), dtype=torch.float32, device=dev)
+        ops.embed(meta.toks, w.embed, x, meta.pos, w.pos_table)
+        for r in g.local_ranks:   # the embedding is replicated: every rank norms all rows
+            ops.add_rmsnorm(x, w.layers[0].attn_gain, eps, peer.xn[r][0][:M])
+
+        def reduce(pi, gain, xi):
+            g.charge("all_reduce", [2.0 * (P - 1) / P * M * h * 4] * P)
+            for r in g.local_ranks:
+                ops.peer_wait(peer.flags[r][2 + pi], P)
+            for r in g.local_ranks:
+                ops.peer_reduce_scatter_rmsnorm(peer.part_ptrs[pi], P, r, x, gain, eps,
+                                                peer.xn_ptrs[xi], h, M)
+            for r in g.local_ranks:
+                ops.peer_signal(peer.ag_flag_ptrs[xi], P, r)
+            for r in g.local_ranks:
+                ops.peer_wait(peer.flags[r][4 + xi], P)
+
+        for layer in range(cfg.n_layers):
+            lw = w.layers[layer]
+            if layer > 0:
+                reduce(1, lw.attn_gain, 0)
+            self._stage_all(layer, batch)
+            for r in g.local_ranks:
+                xn = peer.xn[r][0][:M]
+                q = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
+                if self._fused_qkv_rope(M, hq, hk):
+                    self._qkv_rope(r, layer, xn, lw.wqkv[r * W:(r + 1) * W], q, meta, hq, hk,
+                                   meters[r])
+                else:
+                    qkv = torch.empty((M, W), dtype=torch.bfloat16, device=dev)
+                    ops.gemm(xn, lw.wqkv[r * W:(r + 1) * W], qkv, ops.EPI_STORE_BF16, M=M, N=W,
+                             K=h, lda=h, ldb=h, ldd=W, meter=meters[r])
+                    self._kv_write(r, layer, qkv, q, meta, batch)
+                o = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
+                self._attend(r, layer, q, o, meta, meters[r])
+                ops.gemm(o, lw.wo[:, r * hqw:], peer.part[r][0][:M], ops.EPI_STORE_F32, M=M, N=h,
+                         K=hqw, lda=hqw, ldb=cfg.n_heads * d, ldd=h, meter=meters[r])
+                ops.peer_signal(peer.tp_flag_ptrs[0], P, r)
+            reduce(0, lw.mlp_gain, 1)
+            for r in g.local_ranks:
+                act = torch.empty((M, fl), dtype=torch.bfloat16, device=dev)
+                self._mlp_up(peer.xn[r][1][:M], lw, r, act, M, meters[r])
+                ops.gemm(act, lw.wdown[:, r * fl:], peer.part[r][1][:M], ops.EPI_STORE_F32, M=M,
+                         N=h, K=fl, lda=fl, ldb=cfg.ffn_dim, ldd=h, meter=meters[r])
+                ops.peer_signal(peer.tp_flag_ptrs[1], P, r)
+        reduce(1, w.final_gain, 0)   # final norm, pushed like an attention norm
+        n_rows = M if span_logits else meta.n
+        vs = cfg.vocab_size // P
+        parts = {}
+        for r in g.local_ranks:
+            if span_logits:
+                xf = peer.xn[r][0][:M]
+            else:
+                xf = torch.empty((n_rows, h), dtype=torch.bfloat16, device=dev)
+                ops.gather_rows_bf16(peer.xn[r][0], meta.ends, xf)
+            lg = torch.empty((n_rows, vs), dtype=torch.float32, device=dev)
+            ops.gemm(xf, w.head[r * vs:(r + 1) * vs], lg, ops.EPI_STORE_F32, M=n_rows, N=vs, K=h,
+                     lda=h, ldb=h, ldd=vs, meter=meters[r])
+            parts[r] = lg
+        logits = self._gather_vocab(parts, n_rows)
+        return self._split(logits, meta, span_logits)
 
     def _tp_partial(self, peer, r, which, a, w, M, K, ldb, meter):
         """Rank r's TP partial of a residual projection (O: which=0, down: 1).

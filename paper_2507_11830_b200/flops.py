@@ -128,3 +128,15 @@ def gemm_flops_per_token(cfg) -> int:
     per_layer = 2 * h * (cfg.n_heads + 2 * cfg.kv_heads) * d + 2 * cfg.n_heads * d * h \
         + n_mlp * 2 * h * f
     return per_layer * cfg.n_layers
+
+
+def swiftkv_flop_ratio(cfg, prompt_len: int, cut_layer: Optional[int] = None) -> float:
+    """Prefill FLOP ratio early-exit / standard (reference flops.py:203-215):
+    one request of ``prompt_len`` tokens on one device (TP and SP coincide),
+    ``cut_layer`` defaulting to the halfway cut."""
+    cut = cfg.n_layers // 2 if cut_layer is None else cut_layer
+    shape = PassShape(spans=(prompt_len,), history=(0,))
+    early = sum(flop_count(shape, "tp", cfg, 1, swiftkv_cut=cut))
+    std = sum(flop_count(shape, "tp", cfg, 1))
+    return early / std
+

@@ -23,6 +23,7 @@ EPI_ADD_F32 = 2
 EPI_SWIGLU = 3
 EPI_GELU = 4
 EPI_PARTIAL_F32 = 5  # raw K-split partials [n][M][N], n = gemm_partials(M, N, K)
+GEMM_ORDERED = 0x100  # flag: one ascending-K chain per output (never split-K)
 
 # Optional live per-kernel timing (bench.py roofline): when set to a dict, the
 # wrapped launches record CUDA events on the launching stream plus their
@@ -87,9 +88,10 @@ def device_check() -> int:
 
 def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, epilogue: int, *, M: int, N: int,
          K: int, lda: int, ldb: int, ldd: int, a_kchunk: int = 0, a_chunk_stride: int = 0,
-         peer_width: int = 0, peer_stride: int = 0, meter=None) -> None:
+         peer_width: int = 0, peer_stride: int = 0, meter=None, ordered: bool = False) -> None:
     """D = epi(A[M,K] B[N,K]^T) — see sp_gemm_bf16.  A/B may be views with
-    arbitrary base offsets (zero-copy TP shards)."""
+    arbitrary base offsets (zero-copy TP shards).  ``ordered`` pins the
+    one-chain-per-output regime (split-invariant at any M)."""
     _need(a, torch.bfloat16, "gemm A")
     _need(b, torch.bfloat16, "gemm B")
     if epilogue in (EPI_STORE_BF16, EPI_SWIGLU, EPI_GELU):
@@ -106,8 +108,9 @@ def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, epilogue: int, *, M:
     nbytes = (M * K + N * K) * 2 + M * (N // 2 if epilogue == EPI_SWIGLU else N) * d.element_size()
     with _Timed("gemm", 2 * M * N * K, nbytes):  # (split-K reduce, if any, included)
         rc = lib.sp_gemm_bf16(a.data_ptr(), lda, a_kchunk, a_chunk_stride, b.data_ptr(), ldb,
-                              d.data_ptr(), ldd, M, N, K, epilogue, peer_width, peer_stride,
-                              _stream())
+                              d.data_ptr(), ldd, M, N, K,
+                              epilogue | (GEMM_ORDERED if ordered else 0), peer_width,
+                              peer_stride, _stream())
     _lib.check(rc, "sp_gemm_bf16")
 
 
@@ -133,15 +136,42 @@ def gemm_qkv_rope(a: torch.Tensor, b: torch.Tensor, *, M: int, K: int, lda: int,
     _lib.check(rc, "sp_gemm_bf16_qkv_rope")
 
 
-_gemm_ws: Optional[torch.Tensor] = None
+GEMM_WS_BYTES = 64 << 20
+# Every split-K workspace ever registered stays alive for the life of the
+# process: captured CUDA graphs (decode passes) hold its raw address, so
+# replacing it must never return the old buffer to the caching allocator
+# (ADVICE r1).  One default buffer per device, shared by all engines on it
+# (kernels on one stream run in order).
+_ws_keep: list = []
+_ws_default: dict = {}
+_ws_current: dict = {}
 
 
-def set_gemm_workspace(ws: Optional[torch.Tensor]) -> None:
-    """Register the split-K workspace (kept alive here); None disables split-K."""
-    global _gemm_ws
-    _gemm_ws = ws
+def set_gemm_workspace(ws: Optional[torch.Tensor], device=None) -> None:
+    """Register the split-K workspace of `ws`'s device (or `device` when ws is
+    None: disables split-K there).  Registered buffers are never freed."""
+    dev = torch.device(ws.device if ws is not None else (device or "cuda"))
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
     nbytes = 0 if ws is None else ws.numel() * ws.element_size()
-    _lib.check(_lib.load().sp_gemm_set_workspace(_ptr(ws), nbytes), "sp_gemm_set_workspace")
+    if ws is not None:
+        _ws_keep.append(ws)
+    with torch.cuda.device(idx):
+        _lib.check(_lib.load().sp_gemm_set_workspace(_ptr(ws), nbytes), "sp_gemm_set_workspace")
+    _ws_current[idx] = None if ws is None else ws.data_ptr()
+
+
+def ensure_gemm_workspace(device) -> torch.Tensor:
+    """The device's default split-K workspace, allocated once and (re)registered
+    if something else is registered there."""
+    dev = torch.device(device)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    ws = _ws_default.get(idx)
+    if ws is None:
+        ws = torch.empty(GEMM_WS_BYTES, dtype=torch.uint8, device=torch.device("cuda", idx))
+        _ws_default[idx] = ws
+    if _ws_current.get(idx) != ws.data_ptr():
+        set_gemm_workspace(ws)
+    return ws
 
 
 def gemm_to_peers(a: torch.Tensor, b: torch.Tensor, peer_ptrs: torch.Tensor, *, row_off: int,
@@ -194,6 +224,31 @@ def peer_allreduce_add_rmsnorm(part_ptrs: torch.Tensor, peers: int, x: torch.Ten
         part_ptrs.data_ptr(), peers, slabs, x.data_ptr(), x.stride(0), _ptr(gain), float(eps),
         _ptr(out), 0 if out is None else out.stride(0), rows, x.shape[1], _stream()),
         "sp_peer_allreduce_add_rmsnorm")
+
+
+def peer_reduce_scatter_rmsnorm(part_ptrs: torch.Tensor, peers: int, my_rank: int,
+                                x: torch.Tensor, gain: torch.Tensor, eps: float,
+                                xn_ptrs: torch.Tensor, ldo: int, rows: int) -> None:
+    """Two-shot TP all-reduce: sum my row slice's P partials (ascending rank),
+    add into x, push bf16 RMSNorm rows into every rank's xn buffer."""
+    if rows == 0:
+        return
+    _lib.check(_lib.load().sp_peer_reduce_scatter_rmsnorm(
+        part_ptrs.data_ptr(), peers, my_rank, x.data_ptr(), x.stride(0), gain.data_ptr(),
+        float(eps), xn_ptrs.data_ptr(), ldo, rows, x.shape[1], _stream()),
+        "sp_peer_reduce_scatter_rmsnorm")
+
+
+def gather_rows_bf16(src: torch.Tensor, idx: torch.Tensor, dst: torch.Tensor) -> None:
+    """dst[r] = src[idx[r]] for bf16 rows (16-byte vectors)."""
+    _need(src, torch.bfloat16, "gather src")
+    _need(dst, torch.bfloat16, "gather dst")
+    rows = idx.shape[0]
+    if rows == 0:
+        return
+    _lib.check(_lib.load().sp_gather_rows_bf16(src.data_ptr(), src.stride(0), idx.data_ptr(),
+                                               dst.data_ptr(), dst.stride(0), rows, src.shape[1],
+                                               _stream()), "sp_gather_rows_bf16")
 
 
 def embed(ids: torch.Tensor, table: torch.Tensor, out: torch.Tensor,
@@ -363,6 +418,15 @@ def add_f32(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor) -> None:
                "sp_add_f32")
 
 
+def add_f64(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor) -> None:
+    _need(a, torch.float64, "add a")
+    _need(b, torch.float64, "add b")
+    _need(out, torch.float64, "add out")
+    if a.numel():
+        _lib.check(_lib.load().sp_add_f64(a.data_ptr(), b.data_ptr(), out.data_ptr(), a.numel(),
+                                          _stream()), "sp_add_f64")
+
+
 def argmax(logits: torch.Tensor, idx: torch.Tensor, val: Optional[torch.Tensor] = None) -> None:
     _need(logits, torch.float32, "argmax logits")
     rows, vocab = logits.shape
@@ -379,3 +443,33 @@ def gather_rows(src: torch.Tensor, idx: torch.Tensor, dst: torch.Tensor) -> None
     _lib.check(_lib.load().sp_gather_rows_f32(src.data_ptr(), src.stride(0), idx.data_ptr(),
                                               dst.data_ptr(), dst.stride(0), rows, src.shape[1],
                                               _stream()), "sp_gather_rows_f32")
+
+
+def rms_norm_f32(x: torch.Tensor, gain: torch.Tensor, eps: float, out: torch.Tensor) -> None:
+    """out = gain * x / sqrt(mean(x^2) + eps) per row, f32 (sp_rms_norm_f32)."""
+    _need(x, torch.float32, "rms_norm x")
+    _need(gain, torch.float32, "rms_norm gain")
+    _need(out, torch.float32, "rms_norm out")
+    rows, hidden = x.shape
+    _lib.check(_lib.load().sp_rms_norm_f32(x.data_ptr(), x.stride(0), gain.data_ptr(), float(eps),
+                                           out.data_ptr(), out.stride(0), rows, hidden, _stream()),
+               "sp_rms_norm_f32")
+
+
+def gelu_f32(x: torch.Tensor, out: torch.Tensor) -> None:
+    """tanh-form GeLU, elementwise f32 (sp_gelu_f32); x and out contiguous."""
+    _need(x, torch.float32, "gelu x")
+    _need(out, torch.float32, "gelu out")
+    _lib.check(_lib.load().sp_gelu_f32(x.data_ptr(), out.data_ptr(), x.numel(), _stream()),
+               "sp_gelu_f32")
+
+
+def softmax_rows_f32(x: torch.Tensor, out: torch.Tensor) -> None:
+    """Row softmax with shift-by-max, f32 (sp_softmax_rows_f32)."""
+    _need(x, torch.float32, "softmax x")
+    _need(out, torch.float32, "softmax out")
+    rows, width = x.shape
+    _lib.check(_lib.load().sp_softmax_rows_f32(x.data_ptr(), x.stride(0), out.data_ptr(),
+                                               out.stride(0), rows, width, _stream()),
+               "sp_softmax_rows_f32")
+

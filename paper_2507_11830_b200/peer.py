@@ -3,8 +3,11 @@
 Each rank owns, at addresses every peer knows:
   recv  bf16 [max_tokens, W]           seq->head receive (QKV GEMM epilogue stores here)
   back  bf16 [P * rows_max, hq_l * d]  head->seq receive ([P][rows][w], O-proj A operand)
-  flags int32 [4, P]                   completion flags (fwd, back, tp-attn, tp-mlp)
+  flags int32 [6, P]                   completion flags (fwd, back, tp-attn, tp-mlp,
+                                       two-shot all-gather of xn[0], xn[1])
   part  f32 [2, max_tokens, h]         TP partials (O-proj, down-proj) read by every peer
+  xn    bf16 [2, max_tokens, h]        two-shot TP all-reduce: normed rows pushed by their
+                                       owner rank (attn-norm / final-norm, mlp-norm)
 
 Device tables of the P peers' addresses feed the kernels (sp_gemm_bf16_to_peers,
 sp_peer_scatter_rows, sp_peer_signal).  In-process ranks (LoopbackGroup) use
@@ -41,15 +44,18 @@ class PeerLinks:
         n_back = P * self.rows_max * width_back * 2
         self.hidden = hidden
         n_part = 2 * max_tokens * hidden * 4
-        n_flag = 4 * P * 4
+        n_xn = 2 * max_tokens * hidden * 2
+        n_flag = 6 * P * 4
         self.off_recv, self.off_back = 0, _align(n_recv)
         self.off_part = self.off_back + _align(n_back)
-        self.off_flags = self.off_part + _align(n_part)
+        self.off_xn = self.off_part + _align(n_part)
+        self.off_flags = self.off_xn + _align(n_xn)
         total = self.off_flags + _align(n_flag)
         self.recv: Dict[int, torch.Tensor] = {}
         self.back: Dict[int, torch.Tensor] = {}
         self.flags: Dict[int, torch.Tensor] = {}
         self.part: Dict[int, list] = {}
+        self.xn: Dict[int, list] = {}
         bases: List[int] = [0] * P
         if isinstance(group, LoopbackGroup):
             self._bufs = {}
@@ -98,6 +104,8 @@ class PeerLinks:
         self.fwd_flag_ptrs = table(self.off_flags)
         self.back_flag_ptrs = table(self.off_flags + P * 4)
         self.tp_flag_ptrs = [table(self.off_flags + 2 * P * 4), table(self.off_flags + 3 * P * 4)]
+        self.xn_ptrs = [table(self.off_xn), table(self.off_xn + max_tokens * hidden * 2)]
+        self.ag_flag_ptrs = [table(self.off_flags + 4 * P * 4), table(self.off_flags + 5 * P * 4)]
 
     def _views(self, r: int, buf: torch.Tensor) -> None:
         P = self.P
@@ -106,13 +114,25 @@ class PeerLinks:
         nb = P * self.rows_max * self.w_back
         self.back[r] = buf[self.off_back:self.off_back + nb * 2].view(torch.bfloat16) \
             .view(P * self.rows_max, self.w_back)
-        self.flags[r] = buf[self.off_flags:self.off_flags + 4 * P * 4].view(torch.int32).view(4, P)
+        self.flags[r] = buf[self.off_flags:self.off_flags + 6 * P * 4].view(torch.int32).view(6, P)
         npart = self.max_tokens * self.hidden
         self.part.setdefault(r, [None, None])
         for i in range(2):
             lo = self.off_part + i * npart * 4
             self.part[r][i] = buf[lo:lo + npart * 4].view(torch.float32).view(self.max_tokens,
                                                                               self.hidden)
+        self.xn.setdefault(r, [None, None])
+        for i in range(2):
+            lo = self.off_xn + i * npart * 2
+            self.xn[r][i] = buf[lo:lo + npart * 2].view(torch.bfloat16).view(self.max_tokens,
+                                                                             self.hidden)
+
+
+def two_shot_min_rows() -> int:
+    """TP passes with more rows than this reduce two-shot (reduce-scatter +
+    pushed all-gather); smaller ones (decode batches, graph-captured) keep the
+    one-shot kernel: one launch, one flag round.  SP_TP_TWO_SHOT_MIN_ROWS."""
+    return int(os.environ.get("SP_TP_TWO_SHOT_MIN_ROWS", "256"))
 
 
 def fused_a2a_enabled(group: DeviceGroup) -> bool:

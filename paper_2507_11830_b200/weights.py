@@ -235,3 +235,113 @@ class ModelWeights:
             lw = self.layers[li]
             if lw.wkv is None:
                 lw.wkv = lw.wqkv.index_select(0, idx).contiguous()
+
+
+# ------------------------------------------------- TP shards as views
+@dataclass
+class TpLayerShard:
+    """One layer of a TP rank: zero-copy views of the resident replica."""
+
+    wqkv: torch.Tensor    # rows [rW, (r+1)W) of the fused per-rank q|k|v matrix
+    wo: torch.Tensor      # K window [:, r Hq/P d : (r+1) Hq/P d] (strided view)
+    wgu: torch.Tensor     # rows of the rank's ffn shard (gate|up interleaved, or w1)
+    wdown: torch.Tensor   # K window [:, r f/P : (r+1) f/P]
+
+
+@dataclass
+class TpShard:
+    """What device ``rank`` reads under TP (reference model.py:206-217)."""
+
+    rank: int
+    world_size: int
+    head_range: tuple
+    kv_head_range: tuple
+    vocab_range: tuple
+    ffn_range: tuple
+    layers: List[TpLayerShard]
+    head_rows: torch.Tensor   # [V/P, h] vocab rows of the LM head
+
+
+def tp_shard_view(weights: ModelWeights, rank: int, world_size: Optional[int] = None) -> TpShard:
+    """The blocks device ``rank`` owns under TP (reference model.py:220-254),
+    as views of the one bf16 replica — the same views the engine's TP pass
+    multiplies by (the reference materialises copies)."""
+    from .errors import ContractViolation
+    cfg = weights.config
+    p = weights.world_size if world_size is None else world_size
+    if p != weights.world_size:
+        raise ConfigError(f"weights are laid out for P={weights.world_size}, not {p}")
+    if not 0 <= rank < p:
+        raise ContractViolation(f"rank {rank} out of range for P={p}")
+    d = cfg.head_dim
+    hq, hk, fl, vs = cfg.n_heads // p, cfg.kv_heads // p, cfg.ffn_dim // p, cfg.vocab_size // p
+    W = weights.qkv_width
+    gu = 2 * fl if cfg.mlp == "swiglu" else fl
+    layers = [TpLayerShard(wqkv=lw.wqkv[rank * W:(rank + 1) * W],
+                           wo=lw.wo[:, rank * hq * d:(rank + 1) * hq * d],
+                           wgu=lw.wgu[rank * gu:(rank + 1) * gu],
+                           wdown=lw.wdown[:, rank * fl:(rank + 1) * fl])
+              for lw in weights.layers]
+    return TpShard(rank, p, (rank * hq, (rank + 1) * hq), (rank * hk, (rank + 1) * hk),
+                   (rank * vs, (rank + 1) * vs), (rank * fl, (rank + 1) * fl), layers,
+                   weights.head[rank * vs:(rank + 1) * vs])
+
+
+def _inside(view: torch.Tensor, base: torch.Tensor) -> bool:
+    """view's elements all live inside base's storage (same buffer, in range)."""
+    if view.untyped_storage().data_ptr() != base.untyped_storage().data_ptr():
+        return False
+    lo = view.data_ptr()
+    hi = lo + ((view.shape[0] - 1) * view.stride(0) + (view.shape[1] - 1) * view.stride(1) + 1) \
+        * view.element_size()
+    b_lo = base.data_ptr()
+    return b_lo <= lo and hi <= b_lo + base.numel() * base.element_size()
+
+
+def check_shard_containment(weights: ModelWeights, world_size: Optional[int] = None) -> bool:
+    """Every element of every TP shard is a sub-block of the SP-resident
+    replica (reference model.py:257-281).  Here containment holds by
+    construction — a TP shard IS a view of the replica, no bytes are copied —
+    and is checked structurally: each view aliases the replica's storage at
+    the expected rows / columns."""
+    cfg = weights.config
+    p = weights.world_size if world_size is None else world_size
+    d = cfg.head_dim
+    for rank in range(p):
+        sh = tp_shard_view(weights, rank, p)
+        for lw, sl in zip(weights.layers, sh.layers):
+            if not (_inside(sl.wqkv, lw.wqkv) and _inside(sl.wo, lw.wo)
+                    and _inside(sl.wgu, lw.wgu) and _inside(sl.wdown, lw.wdown)):
+                return False
+            if sl.wo.shape[1] * p != lw.wo.shape[1] or sl.wqkv.shape[0] * p != lw.wqkv.shape[0]:
+                return False
+            if sl.wo.data_ptr() != lw.wo.data_ptr() + rank * (cfg.n_heads // p) * d * 2:
+                return False
+        if not _inside(sh.head_rows, weights.head):
+            return False
+    return True
+
+
+def memory_report(config: ModelConfig, world_size: int) -> dict:
+    """Parameter residency per device (reference model.py:284-300), for the
+    GQA / SwiGLU geometry: matrix parameters shard exactly 1/P under TP; norm
+    gains are replicated.  Shift parallelism keeps the SP replica resident, so
+    ``replica_bytes_per_device`` (bf16) is what each GPU holds; the TP views a
+    TP pass reads are 1/P of it.  Also the per-device KV bytes per token."""
+    c = config
+    h, f, v, L, d = c.hidden, c.ffn_dim, c.vocab_size, c.n_layers, c.head_dim
+    n_mlp = 3 if c.mlp == "swiglu" else 2
+    per_layer = h * (c.n_heads + 2 * c.kv_heads) * d + c.n_heads * d * h + n_mlp * h * f
+    matrix = v * h + L * per_layer + h * v
+    gains = L * 2 * h + h
+    return {
+        "matrix_params_total": matrix,
+        "replicated_gain_params": gains,
+        "sp_matrix_params_per_device": matrix,
+        "tp_matrix_params_per_device": matrix // world_size,
+        "sharded_ratio": world_size,
+        "replica_bytes_per_device": 2 * matrix + 4 * gains,
+        "tp_view_bytes_per_device": 2 * matrix // world_size,
+        "kv_bytes_per_token_per_device": 2 * L * (c.kv_heads // world_size) * d * 2,
+    }
+

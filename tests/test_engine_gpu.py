@@ -440,7 +440,7 @@ def test_cuda_graph_decode_matches_eager(c1, p):
         eng.step(Batch(BatchKind.PREFILL, [BatchItem(s, q) for s, q in zip(seqs, prompts)]))
         outs, recs = [], []
         toks = [1, 2, 3]
-        for step in range(6):
+        for step in range(9):
             sub = seqs if step % 3 != 2 else seqs[:2]  # batch 3 -> SP, batch 2 -> TP (tau=3)
             lg, rec = eng.step(Batch(BatchKind.DECODE, [BatchItem(s, [t]) for s, t in zip(sub, toks)]))
             outs.append([x.cpu() for x in lg])
@@ -449,12 +449,47 @@ def test_cuda_graph_decode_matches_eager(c1, p):
         res[graphs] = (outs, recs, [s.cache.write_counter for s in seqs],
                        [s.cache.token_count for s in seqs])
         if graphs:
-            assert len(eng._graphs) >= 2  # SP and TP keys captured
+            # both keys captured (second sighting) AND replayed at least once
+            by_mode = {k[0]: e for k, e in eng._graphs.items()}
+            for mode in (ParallelMode.SP, ParallelMode.TP):
+                assert by_mode[mode].graph is not None and by_mode[mode].replays >= 1, mode
     (o0, r0, w0, t0), (o1, r1, w1, t1) = res[False], res[True]
     assert r0 == r1 and w0 == w1 and t0 == t1
     for a, b in zip(o0, o1):
         for x, y in zip(a, b):
             assert torch.equal(x, y)
+
+
+def test_graphs_survive_a_second_engine(c1):
+    """captured decode graphs hold the split-K workspace address; a
+    second Engine on the device must not free it.  Replays of engine A after
+    engine B exists equal A's eager passes bit for bit."""
+    prompt = c1_prompts()[0][:40]
+
+    def run(graphs, interleave):
+        eng = Engine(device_weights(c1, 1), LoopbackGroup(1), ShiftPolicy.fixed_tp(),
+                     cuda_graphs=graphs)
+        s = eng.new_sequence(0, capacity=64)
+        eng.step(Batch(BatchKind.PREFILL, [BatchItem(s, prompt)]))
+        outs, tok, other = [], 7, None
+        for step in range(5):
+            if interleave and step == 2:   # after the capture: a second engine appears
+                other = Engine(device_weights(c1, 1), LoopbackGroup(1), ShiftPolicy.fixed_tp())
+                o = other.new_sequence(0, capacity=64)
+                other.step(Batch(BatchKind.PREFILL, [BatchItem(o, prompt[:20])]))
+                other.step(Batch(BatchKind.DECODE, [BatchItem(o, [3])]))
+                torch.cuda.empty_cache()
+            lg, _ = eng.step(Batch(BatchKind.DECODE, [BatchItem(s, [tok])]))
+            outs.append(lg[0].cpu())
+            tok = int(torch.argmax(lg[0]))
+        if graphs:
+            assert sum(e.replays for e in eng._graphs.values()) >= 2
+        return outs
+
+    want = run(False, False)
+    got = run(True, True)
+    for a, b in zip(want, got):
+        assert torch.equal(a, b)
 
 
 @pytest.mark.parametrize("p", [2, 4])
@@ -482,6 +517,39 @@ def test_fused_peer_all_to_all_matches_collective_path(c1_kv4, p, monkeypatch):
     for a, b in zip(res["1"][0], res["0"][0]):
         assert torch.equal(a, b)
     assert res["1"][1] == res["0"][1]
+
+
+@pytest.mark.parametrize("p", [2, 4])
+@pytest.mark.parametrize("span", [False, True])
+def test_two_shot_tp_allreduce_matches_one_shot_and_collective(c1_kv4, p, span, monkeypatch):
+    """Prefill-size TP passes (> SP_TP_TWO_SHOT_MIN_ROWS rows) reduce two-shot:
+    each rank sums its row slice (ascending rank), adds the residual, norms and
+    pushes bf16 rows to every peer.  Bit-identical logits, KV and ledger to the
+    one-shot kernel and to the collective path; uneven row slices (M % P != 0)."""
+    prompts = [c1_prompts()[i] for i in (0, 3, 5)]   # 349 tokens
+    assert sum(len(q) for q in prompts) % p
+    res = {}
+    for name, env in (("two", {}), ("one", {"SP_TP_TWO_SHOT_MIN_ROWS": "100000"}),
+                      ("coll", {"SP_FUSED_A2A": "0"})):
+        for k in ("SP_TP_TWO_SHOT_MIN_ROWS", "SP_FUSED_A2A"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        eng = make(c1_kv4, p)
+        seqs = [eng.new_sequence(i, capacity=200) for i in range(3)]
+        lg, rec = eng.step(Batch(BatchKind.PREFILL, [BatchItem(s, q) for s, q in zip(seqs, prompts)]),
+                           mode=ParallelMode.TP, span_logits=span)
+        lg2, _ = eng.step(Batch(BatchKind.DECODE, [BatchItem(s, [7]) for s in seqs]),
+                          mode=ParallelMode.TP)
+        k_, v_ = seqs[2].cache.read_window(p - 1, 3, 0)
+        res[name] = ([x.cpu() for x in lg + lg2], rec.comm, k_.cpu(), v_.cpu(),
+                     [s.cache.write_counter for s in seqs])
+    for other in ("one", "coll"):
+        for a, b in zip(res["two"][0], res[other][0]):
+            assert torch.equal(a, b), other
+        assert res["two"][1] == res[other][1]
+        assert torch.equal(res["two"][2], res[other][2]) and torch.equal(res["two"][3], res[other][3])
+        assert res["two"][4] == res[other][4]
 
 
 @pytest.mark.parametrize("p", [2, 4])

@@ -267,10 +267,35 @@ def test_attention_split_plan_covers_every_key_tile_once():
     (512, 4096, 2, 128), (512, 6144, 0, 1),                   # wave model at small per-rank M
     (300, 28672, 3, 1), (1, 128256, 1, 256)])                 # SwiGLU forces 256; LM head row
 def test_gemm_plan_regimes(M, N, epi, want, monkeypatch):
-    """The host-side GEMM plan (sp_gemm_plan, the same function sp_gemm_bf16
+    """The host-side GEMM plan (sp_gemm_plan, the one function sp_gemm_bf16
     dispatches on) picks the documented regime per shape on 148 SMs."""
+    import ctypes
+    lib = _lib.load()
     for k in ("SP_GEMM_NO_SPLITK", "SP_GEMM_FORCE_BN", "SP_GEMM_2CTA"):
         monkeypatch.delenv(k, raising=False)
-    assert _lib.load().sp_gemm_plan(M, N, 4096, epi, 148) == want
-    monkeypatch.setenv("SP_GEMM_NO_SPLITK", "1")  # tests pin the non-decode regime this way
-    assert _lib.load().sp_gemm_plan(M, N, 4096, epi, 148) != 0
+    # a registered split-K workspace (address only: planning never touches it)
+    assert lib.sp_gemm_set_workspace(ctypes.c_void_p(1 << 24), 64 << 20) == 0
+    try:
+        assert lib.sp_gemm_plan(M, N, 4096, epi, 148) == want
+        monkeypatch.setenv("SP_GEMM_NO_SPLITK", "1")  # tests pin the non-decode regime this way
+        assert lib.sp_gemm_plan(M, N, 4096, epi, 148) != 0
+    finally:
+        lib.sp_gemm_set_workspace(None, 0)
+
+
+def test_gemm_plan_follows_dispatch_overrides(monkeypatch):
+    """the plan reports what the dispatcher runs — no workspace
+    means no K-split swap-AB (raw partials need none), and FORCE_BN=256 with
+    SP_GEMM_2CTA=0 is a 1-CTA 128x256 tile, not a pair."""
+    lib = _lib.load()
+    for k in ("SP_GEMM_NO_SPLITK", "SP_GEMM_FORCE_BN", "SP_GEMM_2CTA"):
+        monkeypatch.delenv(k, raising=False)
+    lib.sp_gemm_set_workspace(None, 0)
+    assert lib.sp_gemm_partials(1, 4096, 4096) > 1
+    assert lib.sp_gemm_plan(1, 4096, 4096, 1, 148) != 0     # split-K swap needs the workspace
+    assert lib.sp_gemm_plan(1, 4096, 4096, 5, 148) == 0     # partial epilogue writes into D
+    monkeypatch.setenv("SP_GEMM_FORCE_BN", "256")
+    monkeypatch.setenv("SP_GEMM_2CTA", "0")
+    assert lib.sp_gemm_plan(8192, 6144, 4096, 0, 148) == 256
+    monkeypatch.delenv("SP_GEMM_2CTA")
+    assert lib.sp_gemm_plan(8192, 6144, 4096, 0, 148) == 1
