@@ -471,7 +471,7 @@ def run_ours(args):
         # decode streams the layer weights + LM head (the embedding table is
         # only gathered: B rows) and every request's KV window
         wbytes = weights.nbytes() - weights.embed.nbytes
-        tau = default_token_threshold(world)
+        tau = default_token_threshold(world, cfg)   # B200 crossover (shift_cost)
         for B in sorted({1, dec_b}):
             seqs = [eng.new_sequence(100 + 1000 * B + i, capacity=args.decode_ctx + 64)
                     for i in range(B)]
@@ -511,7 +511,8 @@ def run_ours(args):
                                    "frac_hbm_roofline": round(roof / tpot, 4),
                                    "bytes_per_step": wb + kv_bytes}
             m_shift = choose_mode(ShiftPolicy(token_threshold=tau), dbatch())
-            row["shift"] = {"tau": tau, "picks": m_shift.value, **row[m_shift.value]}
+            row["shift"] = {"tau": tau, "tau_reference_4P": default_token_threshold(world),
+                            "picks": m_shift.value, **row[m_shift.value]}
             if world == 1:
                 row["note"] = "P=1: TP and SP are the same single-device computation"
             decode_cells[f"b{B}"] = row

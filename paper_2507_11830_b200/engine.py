@@ -119,9 +119,17 @@ class ShiftPolicy:
         return ShiftPolicy(kind="fixed_sp")
 
 
-def default_token_threshold(world_size: int) -> int:
-    """The reference default 4·P (:130-131); see DESIGN.md for the B200 crossover."""
-    return 4 * world_size
+def default_token_threshold(world_size: int, config=None) -> int:
+    """Without a model config: the reference default 4·P (:130-131).  With
+    one: the B200 crossover of ``shift_cost.crossover`` — the smallest
+    batched-token count from which an SP pass is modelled no slower than a TP
+    pass on this geometry (calibrated by tools/tau_sweep.py)."""
+    if world_size < 1:
+        raise ConfigError("world_size must be >= 1")
+    if config is None:
+        return 4 * world_size
+    from .shift_cost import crossover
+    return max(1, crossover(config, world_size))
 
 
 def choose_mode(policy: ShiftPolicy, batch: Batch) -> ParallelMode:

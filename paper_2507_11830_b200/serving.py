@@ -15,6 +15,14 @@ FLOP/byte clock replaced by real time:
   nearest-rank percentiles (:523-560); finished sequences release their
   paged KV blocks.
 
+With a ``CostModel`` the driver runs on the reference's LOGICAL clock instead
+(serving.py:226-244: each pass advances simulated time by
+flops_max_device / device_flops_per_s + sum over collectives of
+bytes / link_bytes_per_s + latency): arrivals are admitted against simulated
+time, an idle driver jumps to the next arrival, and no wall time is read — the
+pass schedule is then a deterministic function of the trace, the policy and
+the step records, directly comparable with ``run_serving_loop``.
+
 Trace files use the reference's JSON-lines format (arrival_ms, prompt_len,
 output_len, corpus), so reference traces replay unchanged.
 """
@@ -101,6 +109,26 @@ def prompt_tokens(entry: TraceEntry, vocab_size: int, seed: int) -> List[int]:
     return (tpl * (-(-entry.prompt_len // ell)))[:entry.prompt_len]
 
 
+@dataclass(frozen=True)
+class CostModel:
+    """Deterministic pass-time model (reference serving.py:226-244): the
+    logical clock of a replay.  Defaults are the reference's."""
+
+    device_flops_per_s: float = 1.0e10
+    link_bytes_per_s: float = 1.0e9
+    collective_latency_s: float = 5.0e-5
+
+    def validate(self) -> "CostModel":
+        if min(self.device_flops_per_s, self.link_bytes_per_s, self.collective_latency_s) <= 0:
+            raise ContractViolation("cost model parameters must be positive")
+        return self
+
+    def step_time_s(self, record) -> float:
+        compute = record.flops_max_device / self.device_flops_per_s
+        comm = sum(e.bytes / self.link_bytes_per_s + self.collective_latency_s for e in record.comm)
+        return compute + comm
+
+
 @dataclass
 class RequestMetrics:
     request_id: int
@@ -121,6 +149,8 @@ class PassLog:
     batch_tokens: int
     n_requests: int
     pass_ms: float
+    flops: int = 0          # record.flops_total (reference StepLogEntry.flops)
+    comm_bytes: float = 0.0  # record.comm_bytes (reference StepLogEntry.bytes)
 
 
 @dataclass
@@ -142,8 +172,10 @@ class _Live:
 
 
 def run_serving(engine: Engine, trace: Sequence[TraceEntry], seed: int = 0,
-                time_scale: float = 1.0, max_prefill_tokens: Optional[int] = None) -> ServingResult:
-    """Serve a trace to completion on the wall clock.
+                time_scale: float = 1.0, max_prefill_tokens: Optional[int] = None,
+                cost_model: Optional[CostModel] = None) -> ServingResult:
+    """Serve a trace to completion on the wall clock, or on the logical clock
+    of ``cost_model`` (reference run_serving_loop semantics, serving.py:311-517).
 
     ``time_scale`` stretches (>1) or compresses (<1) the trace's arrival times;
     ``max_prefill_tokens`` optionally caps the tokens of one prefill pass
@@ -165,6 +197,9 @@ def run_serving(engine: Engine, trace: Sequence[TraceEntry], seed: int = 0,
     passes: List[PassLog] = []
     outputs: Dict[int, List[int]] = {}
     t0 = time.perf_counter()
+    if cost_model is not None:
+        cost_model.validate()
+    sim = [0.0]  # logical clock (ms), used when cost_model is set
     nxt = 0
     pool_blocks = engine.pool.alloc.num_blocks
     bsz = engine.pool.block_size
@@ -174,6 +209,8 @@ def run_serving(engine: Engine, trace: Sequence[TraceEntry], seed: int = 0,
         return -(-(len(r.prompt) + r.entry.output_len - 1) // bsz)
 
     def now_ms() -> float:
+        if cost_model is not None:
+            return sim[0]
         return (time.perf_counter() - t0) * 1e3
 
     def done(r: _Live) -> None:
@@ -200,7 +237,9 @@ def run_serving(engine: Engine, trace: Sequence[TraceEntry], seed: int = 0,
             if nxt >= len(arrivals):
                 break
             wait = arrivals[nxt].entry.arrival_ms * time_scale - now_ms()
-            if wait > 0:
+            if cost_model is not None:
+                sim[0] = max(sim[0], arrivals[nxt].entry.arrival_ms * time_scale)
+            elif wait > 0:
                 time.sleep(wait / 1e3)
             continue
         take = []
@@ -232,6 +271,8 @@ def run_serving(engine: Engine, trace: Sequence[TraceEntry], seed: int = 0,
         t_pass = now_ms()
         logits, rec = engine.step(batch, mode=mode)
         ids = greedy_tokens(logits)  # one argmax kernel + one D2H: the pass is complete
+        if cost_model is not None:
+            sim[0] += cost_model.step_time_s(rec) * 1000.0
         t_end = now_ms()
         for r, tok in zip(take, ids):
             r.tokens.append(tok)
@@ -249,7 +290,7 @@ def run_serving(engine: Engine, trace: Sequence[TraceEntry], seed: int = 0,
         if kind == "decode":
             decoding = still
         passes.append(PassLog(rec.step_id, t_end, rec.mode.value, kind, rec.new_tokens,
-                              rec.n_requests, t_end - t_pass))
+                              rec.n_requests, t_end - t_pass, rec.flops_total, rec.comm_bytes))
     metrics.sort(key=lambda m: m.request_id)
     return ServingResult(metrics, passes, rejected, outputs)
 

@@ -299,3 +299,27 @@ def test_gemm_plan_follows_dispatch_overrides(monkeypatch):
     assert lib.sp_gemm_plan(8192, 6144, 4096, 0, 148) == 256
     monkeypatch.delenv("SP_GEMM_2CTA")
     assert lib.sp_gemm_plan(8192, 6144, 4096, 0, 148) == 1
+
+
+def test_b200_crossover_model():
+    """default_token_threshold with a geometry = the B200 cost-model crossover
+    (shift_cost): TP wins decode-size passes, SP wins long prefills, tau grows
+    with P (SP's replica streaming is P x TP's shard), and the reference's 4P
+    stays the geometry-free default."""
+    from paper_2507_11830_b200 import llama31_8b, llama33_70b
+    from paper_2507_11830_b200.shift_cost import comm_us, crossover, pass_us
+    for cfg in (llama31_8b(), llama33_70b()):
+        taus = [default_token_threshold(p, cfg) for p in (2, 4, 8)]
+        assert taus == sorted(taus) and taus[0] > 4 * 2
+        assert default_token_threshold(1, cfg) == 1
+        for p, tau in zip((2, 4, 8), taus):
+            assert tau == crossover(cfg, p)
+            for m in (1, 8, 64):
+                assert pass_us(cfg, "tp", p, m) < pass_us(cfg, "sp", p, m)
+            for m in (tau, 2 * tau, 8192, 32768):
+                assert pass_us(cfg, "sp", p, m) <= pass_us(cfg, "tp", p, m)
+            # SP moves ~P x fewer collective bytes than TP at prefill sizes
+            assert comm_us(cfg, "sp", p, 8192) < comm_us(cfg, "tp", p, 8192)
+    assert default_token_threshold(8) == 32
+    with pytest.raises(ConfigError):
+        default_token_threshold(0)
