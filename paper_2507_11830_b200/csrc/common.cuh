@@ -279,6 +279,29 @@ __device__ __forceinline__ float rms_chunk_sum(const float (&ssq)[VEC], int hidd
   return red[0];
 }
 
+// Row-norm arithmetic shared by every RMSNorm kernel (add_rmsnorm and the
+// fused TP all-reduce variants), with the rounding pinned — no FMA
+// contraction, which nvcc applies per call site — so the fused kernels are
+// bit-identical to the plain one by construction.
+__device__ __forceinline__ float norm_sq4(float4 t) {
+  return __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(t.x, t.x), __fmul_rn(t.y, t.y)),
+                             __fmul_rn(t.z, t.z)),
+                   __fmul_rn(t.w, t.w));
+}
+
+__device__ __forceinline__ float norm_den(float ss, int hidden, float eps) {
+  return sqrtf(__fadd_rn(__fdiv_rn(ss, (float)hidden), eps));
+}
+
+// bf16x4 of gain * (v / den)
+__device__ __forceinline__ uint2 norm_pack4(float4 g, float v0, float v1, float v2, float v3,
+                                            float den) {
+  uint2 u;
+  u.x = pack_bf16x2(__fmul_rn(g.x, __fdiv_rn(v0, den)), __fmul_rn(g.y, __fdiv_rn(v1, den)));
+  u.y = pack_bf16x2(__fmul_rn(g.z, __fdiv_rn(v2, den)), __fmul_rn(g.w, __fdiv_rn(v3, den)));
+  return u;
+}
+
 // Block size of the norm kernels: one float4 per thread (up to 1024 threads)
 // for few rows (decode: one CTA per row, loads spread wide), 256-thread
 // blocks for many rows (prefill) — measured: 1024 costs ~2.5% of an 8K

@@ -124,20 +124,18 @@ __global__ void peer_allreduce_norm_kernel(const unsigned long long* __restrict_
     v[4 * i + 1] = t.y;
     v[4 * i + 2] = t.z;
     v[4 * i + 3] = t.w;
-    ssq[i] = ((t.x * t.x + t.y * t.y) + t.z * t.z) + t.w * t.w;
+    ssq[i] = norm_sq4(t);
   }
   if (out == nullptr) return;
   __shared__ float red[256];
-  const float den = sqrtf(rms_chunk_sum<VEC>(ssq, hidden, red) / (float)hidden + eps);
+  const float den = norm_den(rms_chunk_sum<VEC>(ssq, hidden, red), hidden, eps);
   __nv_bfloat16* orow = out + (int64_t)r * ldo;
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
     const int c = (i * blockDim.x + threadIdx.x) * 4;
     if (c < hidden) {
       const float4 g = *reinterpret_cast<const float4*>(gain + c);
-      uint2 u;
-      u.x = pack_bf16x2(g.x * (v[4 * i + 0] / den), g.y * (v[4 * i + 1] / den));
-      u.y = pack_bf16x2(g.z * (v[4 * i + 2] / den), g.w * (v[4 * i + 3] / den));
+      const uint2 u = norm_pack4(g, v[4 * i + 0], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3], den);
       *reinterpret_cast<uint2*>(orow + c) = u;
     }
   }
@@ -192,18 +190,16 @@ __global__ void peer_reduce_scatter_norm_kernel(const unsigned long long* __rest
     v[4 * i + 1] = t.y;
     v[4 * i + 2] = t.z;
     v[4 * i + 3] = t.w;
-    ssq[i] = ((t.x * t.x + t.y * t.y) + t.z * t.z) + t.w * t.w;
+    ssq[i] = norm_sq4(t);
   }
   __shared__ float red[256];
-  const float den = sqrtf(rms_chunk_sum<VEC>(ssq, hidden, red) / (float)hidden + eps);
+  const float den = norm_den(rms_chunk_sum<VEC>(ssq, hidden, red), hidden, eps);
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
     const int c = (i * blockDim.x + threadIdx.x) * 4;
     if (c < hidden) {
       const float4 g = *reinterpret_cast<const float4*>(gain + c);
-      uint2 u;
-      u.x = pack_bf16x2(g.x * (v[4 * i + 0] / den), g.y * (v[4 * i + 1] / den));
-      u.y = pack_bf16x2(g.z * (v[4 * i + 2] / den), g.w * (v[4 * i + 3] / den));
+      const uint2 u = norm_pack4(g, v[4 * i + 0], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3], den);
       for (int s = 0; s < peers; ++s)
         *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(xn_ptrs[s]) +
                                   (int64_t)r * ldo + c) = u;

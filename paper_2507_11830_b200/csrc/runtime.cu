@@ -123,19 +123,17 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, int64_t ldx, const flo
     v[4 * i + 1] = t.y;
     v[4 * i + 2] = t.z;
     v[4 * i + 3] = t.w;
-    ssq[i] = ((t.x * t.x + t.y * t.y) + t.z * t.z) + t.w * t.w;
+    ssq[i] = norm_sq4(t);
   }
   __shared__ float red[256];
   const float ss = rms_chunk_sum<VEC>(ssq, hidden, red);
-  const float den = sqrtf(ss / (float)hidden + eps);
+  const float den = norm_den(ss, hidden, eps);
   __nv_bfloat16* orow = out + (int64_t)r * ldo;
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
     const int c = (i * blockDim.x + threadIdx.x) * 4;
     if (c < hidden) {
-      uint2 u;
-      u.x = pack_bf16x2(g[i].x * (v[4 * i + 0] / den), g[i].y * (v[4 * i + 1] / den));
-      u.y = pack_bf16x2(g[i].z * (v[4 * i + 2] / den), g[i].w * (v[4 * i + 3] / den));
+      const uint2 u = norm_pack4(g[i], v[4 * i + 0], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3], den);
       *reinterpret_cast<uint2*>(orow + c) = u;
     }
   }
