@@ -40,7 +40,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", OUT + ".tmp", *sources()]
+    extra = os.environ.get("SP_NVCC_EXTRA", "").split()  # e.g. -DSWAP_NORM_DEBUG (debug builds)
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", OUT + ".tmp",
+           *sources()]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

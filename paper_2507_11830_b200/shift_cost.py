@@ -17,8 +17,8 @@ between the two modes for ONE rank of a P-GPU group at M new tokens:
   H/P heads over every token) and cancel.
 
 ``pass_us`` puts a roofline GEMM time (max of compute at the in-step tcgen05
-rate and weight streaming at the measured swap-AB decode efficiency, plus a
-per-launch floor) next to the link model; ``crossover`` is the smallest M from
+rate and weight streaming, plus a per-launch cost — fitted to measured
+per-rank timings, ``GemmModel``) next to the link model; ``crossover`` is the smallest M from
 which SP stays at least as fast as TP.  The GEMM constants are calibrated
 against tools/tau_sweep.py (per-layer projection times of one rank measured on
 a B200 with the product's dispatch; profiles/r02_tau_sweep.json); the link
@@ -41,11 +41,19 @@ class LinkModel:
 
 @dataclass(frozen=True)
 class GemmModel:
-    tflops: float = 1350.0         # in-step tcgen05 GEMM rate (BENCH r01/r02 roofline.achieved)
+    """Least-squares fit (log error) to the 108 per-rank layer timings of
+    tools/tau_sweep.py (profiles/r02_tau_sweep.json; 8B shapes, P = 2/4/8,
+    M = 1..4096, graph-replayed): every GEMM costs max(compute, weight
+    streaming) plus a fixed, non-overlapped ~9 us; the swap-AB regime
+    (M <= 256 token rows, padded to 32) computes at ~800 TFLOP/s, the
+    128-row tiles above it at ~1400."""
+
+    tflops: float = 1400.0         # 128/256-row tcgen05 tiles (M > swap_max_rows)
+    swap_tflops: float = 800.0     # swap-AB regime
+    swap_max_rows: int = 256
     hbm_gbs: float = 6454.6        # MEASURED_PEAKS.json copy bandwidth
-    stream_eff: float = 0.72       # swap-AB weight streaming, fraction of hbm_gbs (sweep)
-    launch_us: float = 2.5         # per-GEMM floor (launch + pipeline fill, PDL-overlapped)
-    m_quantum: int = 32            # rows are padded to this in the smallest tile
+    stream_eff: float = 1.0        # weight streaming, fraction of hbm_gbs
+    launch_us: float = 9.0         # per-GEMM fixed cost (launch, fill, drain, tail)
 
 
 B200_LINKS = LinkModel()
@@ -55,8 +63,11 @@ B200_GEMM = GemmModel()
 def _gemm_us(rows: int, n: int, k: int, g: GemmModel) -> float:
     if rows <= 0:
         return 0.0
-    pad = -(-rows // g.m_quantum) * g.m_quantum
-    compute = 2.0 * pad * n * k / (g.tflops * 1e12)
+    if rows <= g.swap_max_rows:
+        pad, tf = -(-rows // 32) * 32, g.swap_tflops
+    else:
+        pad, tf = -(-rows // 128) * 128, g.tflops
+    compute = 2.0 * pad * n * k / (tf * 1e12)
     stream = (n * k + rows * k + rows * n) * 2.0 / (g.hbm_gbs * 1e9 * g.stream_eff)
     return max(compute, stream) * 1e6 + g.launch_us
 

@@ -303,14 +303,15 @@ def test_gemm_plan_follows_dispatch_overrides(monkeypatch):
 
 def test_b200_crossover_model():
     """default_token_threshold with a geometry = the B200 cost-model crossover
-    (shift_cost): TP wins decode-size passes, SP wins long prefills, tau grows
-    with P (SP's replica streaming is P x TP's shard), and the reference's 4P
-    stays the geometry-free default."""
+    (shift_cost): TP wins decode-size passes, SP wins every pass from tau up,
+    tau sits between the reference's 4P and one 8K prefill, and 4P stays the
+    geometry-free default.  (tau is not monotone in P: the GEMM regime and the
+    one-/two-shot all-reduce switch at fixed row counts.)"""
     from paper_2507_11830_b200 import llama31_8b, llama33_70b
     from paper_2507_11830_b200.shift_cost import comm_us, crossover, pass_us
     for cfg in (llama31_8b(), llama33_70b()):
         taus = [default_token_threshold(p, cfg) for p in (2, 4, 8)]
-        assert taus == sorted(taus) and taus[0] > 4 * 2
+        assert all(4 * p < t <= 8192 for p, t in zip((2, 4, 8), taus))
         assert default_token_threshold(1, cfg) == 1
         for p, tau in zip((2, 4, 8), taus):
             assert tau == crossover(cfg, p)
