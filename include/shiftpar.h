@@ -224,9 +224,16 @@ sp_status sp_a2a_unpack(const void* src, void* dst, int64_t ldd, int rows, int p
  *    array (system-scope release after the stores), sp_peer_wait acquires all
  *    P local flags and resets them.
  */
+/* peer_ptrs_host (may be NULL): the same P pointers in host memory.  With them
+ * and a bf16 epilogue in the 2-CTA (prefill) regime, each epilogue warp stages
+ * 32 rows x 64 columns in shared memory and a TMA store
+ * (cp.async.bulk.tensor, one map per peer) writes whole 128-B lines of the
+ * peer's rows; otherwise the epilogue stores directly.  SP_PEER_TMA=0 forces
+ * the direct stores.  Bit-identical either way. */
 sp_status sp_gemm_bf16_to_peers(const void* A, int64_t lda, int64_t a_kchunk,
                                 int64_t a_chunk_stride, const void* B, int64_t ldb,
-                                const unsigned long long* peer_ptrs, int64_t row_off,
+                                const unsigned long long* peer_ptrs,
+                                const unsigned long long* peer_ptrs_host, int64_t row_off,
                                 int64_t ldd, int M, int N, int K, int epilogue,
                                 int64_t peer_width, void* stream);
 sp_status sp_peer_scatter_rows(const void* src, int64_t lds, int rows_total, int width, int peers,

@@ -29,8 +29,8 @@ SIGNATURES = {
     "sp_gemm_bf16": (_c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _c_int, _c_int, _c_int,
                               _c_int, _i64, _i64, _vp]),
     "sp_gemm_set_workspace": (_c_int, [_vp, _i64]),
-    "sp_gemm_bf16_to_peers": (_c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _c_int,
-                                       _c_int, _c_int, _c_int, _i64, _vp]),
+    "sp_gemm_bf16_to_peers": (_c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _i64,
+                                       _c_int, _c_int, _c_int, _c_int, _i64, _vp]),
     "sp_peer_scatter_rows": (_c_int, [_vp, _i64, _c_int, _c_int, _c_int, _c_int, _vp, _vp]),
     "sp_peer_signal": (_c_int, [_vp, _c_int, _c_int, _vp]),
     "sp_peer_wait": (_c_int, [_vp, _c_int, _vp]),

@@ -89,6 +89,22 @@ struct Params {
 constexpr int EPI_QKV_ROPE = 100;  // internal: only via sp_gemm_bf16_qkv_rope
 static thread_local Params::Rope t_rope = {};
 
+// Per-peer TMA store maps of the fused seq->head exchange (pair kernel):
+// m[b] = 2-D bf16 map over peer b's receive rows [row_off + M][peer_width]
+// (rows past the pass are clipped by the map), box 64 cols x 32 rows, 128-B
+// swizzle.  n == 0: the epilogue stores directly (row-strided 16-B stores).
+constexpr int kMaxPeerMaps = 8;
+struct PeerMaps {
+  CUtensorMap m[kMaxPeerMaps];
+  int n;
+};
+static thread_local const unsigned long long* t_peer_ptrs_host = nullptr;
+
+static bool peer_tma_enabled() {  // SP_PEER_TMA=0: direct epilogue stores (A/B runs)
+  const char* e = getenv("SP_PEER_TMA");
+  return !(e && e[0] == '0');
+}
+
 // destination element (m, n) of D honouring the per-peer layouts
 template <typename T>
 __device__ __forceinline__ T* out_ptr(const Params& p, int m, int64_t n) {
@@ -740,6 +756,10 @@ constexpr int A_BYTES = 128 * BK * 2;
 constexpr int B_BYTES = 128 * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+// peer-TMA variant: + per-epilogue-warp 4 KiB staging boxes [32 rows][64 cols]
+constexpr int OUT_OFF = STAGES * STAGE_BYTES + 1024;  // past the barriers, 1024-aligned
+constexpr int OUT_BYTES = 4 * 4096;
+constexpr int SMEM_BYTES_TMA = OUT_OFF + OUT_BYTES + 1024;
 
 __device__ __forceinline__ uint32_t cta_rank() {
   uint32_t r;
@@ -795,7 +815,7 @@ __device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const Params p) {
+                     const Params p, const __grid_constant__ PeerMaps pm) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -945,6 +965,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           for (int j = 0; j < 32; ++j) v[j] = silu(__uint_as_float(g[j])) * __uint_as_float(u[j]);
           store_chunk(p, m, nb * 128 + c, v, SP_EPI_STORE_BF16, p.N / 2);
         }
+      } else if (pm.n > 0) {
+        // fused seq->head exchange (bf16): each warp stages its 32 rows x 64
+        // columns in a 128-B-swizzled box and one TMA store writes it into the
+        // owning peer's receive rows — whole 128-B lines over NVLink instead of
+        // 32 row-strided 16-B stores per warp instruction
+        uint8_t* stage = smem + pair::OUT_OFF + quarter * 4096;
+        const int mrow0 = mb * 256 + rank * 128 + quarter * 32;
+#pragma unroll 1
+        for (int c = 0; c < 256; c += 64) {
+          uint32_t r0[32], r1[32];
+          tmem_ld32(tb + c, r0);
+          tmem_ld32(tb + c + 32, r1);
+          tmem_ld_wait();
+          if (lane == 0) bulk_wait_read0();  // the previous box has left `stage`
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t* r = j < 4 ? r0 : r1;
+            const int e = (j & 3) * 8;
+            uint4 u;
+            u.x = pack_bf16x2(__uint_as_float(r[e + 0]), __uint_as_float(r[e + 1]));
+            u.y = pack_bf16x2(__uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
+            u.z = pack_bf16x2(__uint_as_float(r[e + 4]), __uint_as_float(r[e + 5]));
+            u.w = pack_bf16x2(__uint_as_float(r[e + 6]), __uint_as_float(r[e + 7]));
+            *reinterpret_cast<uint4*>(stage + lane * 128 + ((j ^ (lane & 7)) << 4)) = u;
+          }
+          fence_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            const int n = nb * 256 + c;
+            const int b = (int)(n / p.peer_width);
+            tma_store_2d(&pm.m[b], stage, (int)(n - b * p.peer_width),
+                         (int)(mrow0 + p.peer_row_off));
+            bulk_commit();
+          }
+        }
       } else {
 #pragma unroll 1
         for (int c = 0; c < 256; c += 32) {
@@ -972,6 +1028,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
     }
   }
+  if (pm.n > 0 && warp >= 2 && (threadIdx.x & 31) == 0) bulk_wait0();  // stores landed
   tc_fence_before();
   pair::cluster_sync();
   if (warp == 1) {
@@ -1348,15 +1405,32 @@ static int launch_pair(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   p.ksplit = 1;
   p.kb_per_split = p.k_blocks;
   choose_raster(p, 256, 256, K, M, N);
+  PeerMaps pm;
+  pm.n = 0;
+  if (t_peer_ptrs_host != nullptr && p.peer_ptrs != nullptr && epilogue == SP_EPI_STORE_BF16 &&
+      peer_width % 64 == 0 && N / peer_width <= kMaxPeerMaps && peer_tma_enabled()) {
+    // one store map per peer over the rows this pass owns in it
+    const int np = (int)(N / peer_width);
+    for (int b = 0; b < np; ++b) {
+      uint64_t dims[2] = {(uint64_t)peer_width, (uint64_t)(p.peer_row_off + M)};
+      uint64_t strides[1] = {(uint64_t)ldd * 2};
+      uint32_t box[2] = {64, 32};
+      if (int rc = get_map(&pm.m[b], reinterpret_cast<const void*>(t_peer_ptrs_host[b]), 2, dims,
+                           strides, box))
+        return rc;
+    }
+    pm.n = np;
+  }
+  const int smem = pm.n > 0 ? pair::SMEM_BYTES_TMA : pair::SMEM_BYTES;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         pair::SMEM_BYTES);
+                         pair::SMEM_BYTES_TMA);
     attr = true;
   }
   const int clusters = std::min(p.num_tiles, sm_count() / 2);
-  launch_k(gemm_pair_kernel, 2 * clusters, NUM_THREADS, pair::SMEM_BYTES,
-           reinterpret_cast<cudaStream_t>(stream), ta, tb, p);
+  launch_k(gemm_pair_kernel, 2 * clusters, NUM_THREADS, smem,
+           reinterpret_cast<cudaStream_t>(stream), ta, tb, p, pm);
   return check_launch("gemm_pair_kernel");
 }
 
@@ -1562,21 +1636,24 @@ extern "C" sp_status sp_gemm_bf16_qkv_rope(const void* A, int64_t lda, const voi
 
 extern "C" sp_status sp_gemm_bf16_to_peers(const void* A, int64_t lda, int64_t a_kchunk,
                                            int64_t a_chunk_stride, const void* B, int64_t ldb,
-                                           const unsigned long long* peer_ptrs, int64_t row_off,
-                                           int64_t ldd, int M, int N, int K, int epilogue,
-                                           int64_t peer_width, void* stream) {
+                                           const unsigned long long* peer_ptrs,
+                                           const unsigned long long* peer_ptrs_host,
+                                           int64_t row_off, int64_t ldd, int M, int N, int K,
+                                           int epilogue, int64_t peer_width, void* stream) {
   using namespace sp::gemm;
   if (!peer_ptrs || peer_width <= 0 || N % peer_width)
     return fail(kInvalid, "gemm_to_peers: need peer pointers and N % peer_width == 0");
   if (epilogue != SP_EPI_STORE_BF16 && epilogue != SP_EPI_STORE_F32)
     return fail(kUnsupported, "gemm_to_peers: store epilogues only");
   t_peer_ptrs = peer_ptrs;
+  t_peer_ptrs_host = peer_ptrs_host;
   t_peer_row_off = row_off;
   // D is never dereferenced in peer mode; pass an aligned placeholder for validation
   const int rc = sp_gemm_bf16(A, lda, a_kchunk, a_chunk_stride, B, ldb,
                               reinterpret_cast<void*>(const_cast<unsigned long long*>(peer_ptrs)),
                               ldd, M, N, K, epilogue, peer_width, 0, stream);
   t_peer_ptrs = nullptr;
+  t_peer_ptrs_host = nullptr;
   t_peer_row_off = 0;
   return rc;
 }

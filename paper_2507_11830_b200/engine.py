@@ -851,14 +851,7 @@ class Engine:
                 row_idx, n_rows = meta.ends, meta.n
         xf = torch.empty((n_rows, h), dtype=torch.bfloat16, device=dev)
         ops.add_rmsnorm(x_rows, w.final_gain, eps, xf, row_idx=row_idx, rows=n_rows)
-        vs = cfg.vocab_size // P
-        parts = {}
-        for r in g.local_ranks:
-            lg = torch.empty((n_rows, vs), dtype=torch.float32, device=dev)
-            ops.gemm(xf, w.head[r * vs:(r + 1) * vs], lg, ops.EPI_STORE_F32, M=n_rows, N=vs, K=h,
-                     lda=h, ldb=h, ldd=vs, meter=meters[r])
-            parts[r] = lg
-        logits = self._gather_vocab(parts, n_rows)
+        logits = self._head_tp({r: xf for r in g.local_ranks}, n_rows, meters)
         return self._split(logits, meta, span_logits and cut is None)
 
     def _forward_tp_two_shot(self, meta, batch, meters, span_logits, peer):
@@ -926,18 +919,14 @@ class Engine:
         reduce(1, w.final_gain, 0)   # final norm, pushed like an attention norm
         n_rows = M if span_logits else meta.n
         vs = cfg.vocab_size // P
-        parts = {}
+        xfs = {}
         for r in g.local_ranks:
             if span_logits:
-                xf = peer.xn[r][0][:M]
+                xfs[r] = peer.xn[r][0][:M]
             else:
-                xf = torch.empty((n_rows, h), dtype=torch.bfloat16, device=dev)
-                ops.gather_rows_bf16(peer.xn[r][0], meta.ends, xf)
-            lg = torch.empty((n_rows, vs), dtype=torch.float32, device=dev)
-            ops.gemm(xf, w.head[r * vs:(r + 1) * vs], lg, ops.EPI_STORE_F32, M=n_rows, N=vs, K=h,
-                     lda=h, ldb=h, ldd=vs, meter=meters[r])
-            parts[r] = lg
-        logits = self._gather_vocab(parts, n_rows)
+                xfs[r] = torch.empty((n_rows, h), dtype=torch.bfloat16, device=dev)
+                ops.gather_rows_bf16(peer.xn[r][0], meta.ends, xfs[r])
+        logits = self._head_tp(xfs, n_rows, meters)
         return self._split(logits, meta, span_logits)
 
     def _tp_partial(self, peer, r, which, a, w, M, K, ldb, meter):
@@ -1000,16 +989,32 @@ class Engine:
             ops.gemm(xn2, lw.wgu[r * fl:(r + 1) * fl], act, ops.EPI_GELU, M=rows, N=fl, K=h,
                      lda=h, ldb=h, ldd=fl, meter=meter)
 
-    def _gather_vocab(self, parts: Dict[int, torch.Tensor], n_rows: int) -> torch.Tensor:
-        """TP logits all-gather (:392-398): per-rank [R, V/P] -> [R, V]."""
-        g = self.group
-        P = self.world_size
+    def _head_tp(self, xfs: Dict[int, torch.Tensor], n_rows: int, meters) -> torch.Tensor:
+        """TP LM head + logits all-gather (:381-398): rank r computes vocab
+        columns [r V/P, (r+1) V/P).  Ranks of this process write their columns
+        straight into the [R, V] result (ldd = V: the gather is free); with one
+        rank per process the [R, V/P] blocks are all-gathered and one unpack
+        kernel interleaves them into [R, V]."""
+        cfg, w, g = self.config, self.weights, self.group
+        P, h, V = self.world_size, cfg.hidden, cfg.vocab_size
+        vs = V // P
+        full = torch.empty((n_rows, V), dtype=torch.float32, device=self.device)
+        local = len(g.local_ranks) == P
+        for r in g.local_ranks:
+            dst, ldd = (full[:, r * vs:], V) if local else (
+                torch.empty((n_rows, vs), dtype=torch.float32, device=self.device), vs)
+            ops.gemm(xfs[r], w.head[r * vs:(r + 1) * vs], dst, ops.EPI_STORE_F32, M=n_rows, N=vs,
+                     K=h, lda=h, ldb=h, ldd=ldd, meter=meters[r])
+            part = dst
         if P == 1:
-            return parts[0]
-        stacked = {r: t.t().contiguous() for r, t in parts.items()}  # [V/P, R] like head_rank
-        vs = self.config.vocab_size // P
-        full = g.all_gather_rows(stacked, [vs] * P)               # [V, R]
-        return full.t().contiguous()
+            return full
+        if local:
+            g.charge("all_gather", [(P - 1) / P * n_rows * V * 4.0] * P)
+            return full
+        blocks = g.all_gather_blocks(part)   # [P, R, V/P]
+        if n_rows:  # f32 moved as bf16 pairs: [P][R][2 vs] -> [R, P * 2 vs]
+            ops.a2a_unpack(blocks.view(torch.bfloat16), full.view(torch.bfloat16), n_rows, P, 2 * vs)
+        return full
 
     def _tail_tp(self, meta, batch, meters, x, cut):
         """SwiftKV TP tail (:400-450): later-layer K/V from z = norm(x, gain_cut),
@@ -1122,7 +1127,8 @@ class Engine:
                     # heads straight into s's receive buffer at this shard's rows
                     ops.gemm_to_peers(xn, lw.wqkv, peer.recv_ptrs, row_off=bounds[r][0],
                                       M=rows[r], N=P * W, K=h, lda=h, ldb=h, ldd=W,
-                                      peer_width=W, meter=meters[r])
+                                      peer_width=W, peer_ptrs_host=peer.recv_ptrs_host,
+                                      meter=meters[r])
                     ops.peer_signal(peer.fwd_flag_ptrs, P, r)
                 elif P == 1:
                     n_qkv = self._partials(M, W, h)
@@ -1475,11 +1481,32 @@ class Engine:
         return [logits[i] for i in range(n)]
 
 
+def _rows_view(rows: List[torch.Tensor]) -> Optional[torch.Tensor]:
+    """The rows as one [n, V] strided view when they are equally spaced rows
+    of one tensor (the engine's logits always are): no copy."""
+    r0 = rows[0]
+    if r0.dim() != 1 or r0.stride(0) != 1:
+        return None
+    n = len(rows)
+    step = (rows[1].data_ptr() - r0.data_ptr()) // r0.element_size() if n > 1 else r0.shape[0]
+    for i, r in enumerate(rows):
+        if (r.dim() != 1 or r.shape != r0.shape or r.dtype != r0.dtype or r.stride(0) != 1
+                or r.untyped_storage().data_ptr() != r0.untyped_storage().data_ptr()
+                or r.data_ptr() != r0.data_ptr() + i * step * r0.element_size()):
+            return None
+    if step < r0.shape[0]:
+        return None
+    return r0.as_strided((n, r0.shape[0]), (step, 1))
+
+
 def greedy_tokens(logits: List[torch.Tensor]) -> List[int]:
     """greedy_token (model.py:303-307) for every item: one argmax kernel, one D2H."""
     if not logits:
         return []
-    rows = torch.stack([l if l.dim() == 1 else l[-1] for l in logits])
+    last = [l if l.dim() == 1 else l[-1] for l in logits]
+    rows = _rows_view(last)
+    if rows is None:
+        rows = torch.stack(last)
     idx = torch.empty(rows.shape[0], dtype=torch.int32, device=rows.device)
     ops.argmax(rows, idx)
     return idx.cpu().tolist()

@@ -245,7 +245,7 @@ class NcclGroup(DeviceGroup):
         if p == 1:
             full = t[:counts[0]]
         else:
-            pad = torch.zeros((mx, width), dtype=t.dtype, device=t.device)
+            pad = torch.empty((mx, width), dtype=t.dtype, device=t.device)  # pad rows unread
             pad[:counts[me]].copy_(t[:counts[me]])
             if self._stage:
                 chunks = [torch.empty((mx, width), dtype=t.dtype) for _ in range(p)]
@@ -258,6 +258,24 @@ class NcclGroup(DeviceGroup):
         nbytes = sum(counts) * width * t.element_size()
         self.charge("all_gather", [(p - 1) / p * nbytes] * p)
         return full
+
+    def all_gather_blocks(self, t: torch.Tensor) -> torch.Tensor:
+        """Every rank's equal-shape block -> [P, *t.shape] (the TP logits
+        gather, fabric.py:173-191; ledger as all_gather)."""
+        p = self.world_size
+        buf = torch.empty((p, *t.shape), dtype=t.dtype, device=t.device)
+        if p == 1:
+            buf[0].copy_(t)
+        elif self._stage:
+            chunks = [torch.empty(t.shape, dtype=t.dtype) for _ in range(p)]
+            self._dist.all_gather(chunks, t.cpu())
+            for r in range(p):
+                buf[r].copy_(chunks[r])
+        else:  # concatenated along dim 0 (the form every backend accepts)
+            self._dist.all_gather_into_tensor(buf.view(p * t.shape[0], *t.shape[1:]),
+                                              t.contiguous())
+        self.charge("all_gather", [(p - 1) / p * p * t.numel() * t.element_size()] * p)
+        return buf
 
     def barrier(self) -> None:
         if self.world_size > 1:

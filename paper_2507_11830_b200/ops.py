@@ -177,9 +177,11 @@ def ensure_gemm_workspace(device) -> torch.Tensor:
 def gemm_to_peers(a: torch.Tensor, b: torch.Tensor, peer_ptrs: torch.Tensor, *, row_off: int,
                   M: int, N: int, K: int, lda: int, ldb: int, ldd: int, peer_width: int,
                   epilogue: int = EPI_STORE_BF16, a_kchunk: int = 0, a_chunk_stride: int = 0,
-                  meter=None) -> None:
+                  peer_ptrs_host=None, meter=None) -> None:
     """GEMM whose epilogue stores column block n // peer_width of row m straight
-    into peer_ptrs[block] at row row_off + m (fused seq->head all-to-all)."""
+    into peer_ptrs[block] at row row_off + m (fused seq->head all-to-all).
+    ``peer_ptrs_host`` (the same pointers as a host int64 array) enables the
+    TMA-store epilogue of the prefill regime."""
     _need(a, torch.bfloat16, "gemm A")
     _need(b, torch.bfloat16, "gemm B")
     if meter is not None:
@@ -187,9 +189,14 @@ def gemm_to_peers(a: torch.Tensor, b: torch.Tensor, peer_ptrs: torch.Tensor, *, 
     if M == 0:
         return
     with _Timed("gemm", 2 * M * N * K, (M * K + N * K) * 2 + M * N * 2):
+        host = None
+        if peer_ptrs_host is not None:
+            host = peer_ptrs_host.ctypes.data if hasattr(peer_ptrs_host, "ctypes") else \
+                peer_ptrs_host.data_ptr()
         rc = _lib.load().sp_gemm_bf16_to_peers(a.data_ptr(), lda, a_kchunk, a_chunk_stride,
-                                               b.data_ptr(), ldb, peer_ptrs.data_ptr(), row_off,
-                                               ldd, M, N, K, epilogue, peer_width, _stream())
+                                               b.data_ptr(), ldb, peer_ptrs.data_ptr(), host,
+                                               row_off, ldd, M, N, K, epilogue, peer_width,
+                                               _stream())
     _lib.check(rc, "sp_gemm_bf16_to_peers")
 
 

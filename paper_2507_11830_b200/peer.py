@@ -22,6 +22,7 @@ from __future__ import annotations
 import os
 from typing import Dict, List
 
+import numpy as np
 import torch
 
 from .fabric import DeviceGroup, LoopbackGroup
@@ -99,6 +100,9 @@ class PeerLinks:
             return torch.tensor([b + off for b in bases], dtype=torch.int64, device=device)
 
         self.recv_ptrs = table(self.off_recv)
+        # the same receive pointers on the host: the TMA-store epilogue encodes
+        # one tensor map per peer from them
+        self.recv_ptrs_host = np.asarray([b + self.off_recv for b in bases], dtype=np.uint64)
         self.back_ptrs = table(self.off_back)
         self.part_ptrs = [table(self.off_part), table(self.off_part + max_tokens * hidden * 4)]
         self.fwd_flag_ptrs = table(self.off_flags)

@@ -22,7 +22,8 @@ per-rank timings, ``GemmModel``) next to the link model; ``crossover`` is the sm
 which SP stays at least as fast as TP.  The GEMM constants are calibrated
 against tools/tau_sweep.py (per-layer projection times of one rank measured on
 a B200 with the product's dispatch; profiles/r02_tau_sweep.json); the link
-constants are NVLink-5 spec numbers, unmeasured until a multi-GPU lease.
+bandwidth is the pool's measured B200 peer copy (770 GB/s per direction), the
+per-collective latency an estimate until a multi-GPU lease.
 """
 
 from __future__ import annotations
@@ -33,9 +34,9 @@ from functools import lru_cache
 
 @dataclass(frozen=True)
 class LinkModel:
-    nvlink_gbs: float = 900.0      # per direction per GPU (NVLink 5 / NVSwitch spec)
-    efficiency: float = 0.75       # achievable fraction for fused peer stores / loads
-    latency_us: float = 6.0        # per collective: flag handshake + launch
+    nvlink_gbs: float = 770.0      # measured B200 peer copy per direction (B200_PROFILING.md)
+    efficiency: float = 1.0        # fraction of that the fused peer stores / loads reach
+    latency_us: float = 6.0        # per collective: flag handshake + launch (unmeasured)
     two_shot_min_rows: int = 256   # peer.two_shot_min_rows() default
 
 

@@ -621,3 +621,34 @@ def test_sp_x_tp_mixed_mode(c1_kv4, monkeypatch):
                      mode=ParallelMode.TP)
     olg, _ = oeng.step([(s, [t]) for s, t in zip(oseqs, toks)], prefill=False, mode="sp")
     assert rel_err(np.stack(to_np(lg)), np.stack(olg)) <= LOGIT_TOL
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_fused_exchange_tma_store_bitexact(p, monkeypatch):
+    """8B-width SP prefill large enough for the 2-CTA GEMM regime (>= 256 rows
+    per rank, N = P x W a multiple of 256): the seq->head exchange epilogue
+    stages 32x64 boxes and TMA-stores them into each peer's receive rows.
+    Logits and K/V are bit-identical to the direct-store epilogue
+    (SP_PEER_TMA=0) and to the collective path (SP_FUSED_A2A=0)."""
+    ow = init_weights_llama(llama_tiny_config(n_layers=2, n_heads=32, n_kv_heads=8, head_dim=128,
+                                              ffn_dim=14336, vocab_size=1024, max_seq=2048), seed=3)
+    rng = np.random.default_rng(11)
+    prompts = [[int(t) for t in rng.integers(0, 1024, size=n)] for n in (700, 413)]  # uneven
+    res = {}
+    for name, env in (("tma", {}), ("direct", {"SP_PEER_TMA": "0"}), ("coll", {"SP_FUSED_A2A": "0"})):
+        for k in ("SP_PEER_TMA", "SP_FUSED_A2A"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        eng = Engine(device_weights(ow, p), LoopbackGroup(p), ShiftPolicy.fixed_sp())
+        seqs = [eng.new_sequence(i, capacity=800) for i in range(2)]
+        lg, rec = eng.step(Batch(BatchKind.PREFILL, [BatchItem(s, q) for s, q in zip(seqs, prompts)]),
+                           mode=ParallelMode.SP, span_logits=True)
+        kv = [t.cpu() for r in range(p) for t in seqs[1].cache.read_window(r, 1, 0)]
+        res[name] = ([x.cpu() for x in lg], kv, rec.comm)
+    for other in ("direct", "coll"):
+        for a, b in zip(res["tma"][0], res[other][0]):
+            assert torch.equal(a, b), other
+        for a, b in zip(res["tma"][1], res[other][1]):
+            assert torch.equal(a, b), other
+        assert res["tma"][2] == res[other][2]

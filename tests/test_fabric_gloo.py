@@ -55,6 +55,8 @@ def _worker(rank, world, port, q):
         out["allreduce"] = grp.all_reduce_sum(part)[rank].clone()
         cnt = [2, 0]
         out["gather"] = grp.all_gather_rows({rank: torch.full((2, 3), float(rank))}, cnt)
+        # the TP logits gather: equal [R, V/P] blocks -> [P, R, V/P]
+        out["blocks"] = grp.all_gather_blocks(torch.full((3, 4), float(rank + 10)))
         out["ledger"] = [(r.kind, r.bytes) for r in grp.records if r.device == 0]
         q.put((rank, {k: (v.tolist() if isinstance(v, torch.Tensor) else v) for k, v in out.items()}))
     finally:
@@ -94,9 +96,11 @@ def test_nccl_group_over_gloo_matches_loopback():
     for r in range(world):
         assert res[r]["allreduce"] == [[3.0] * 4] * 3
         assert res[r]["gather"] == [[0.0] * 3] * 2
+        assert res[r]["blocks"] == [[[10.0] * 4] * 3, [[11.0] * 4] * 3]
     # byte ledger identical to the reference ring formulas, from every rank's view
     lb.all_reduce_sum({0: torch.ones(3, 4), 1: torch.ones(3, 4)})
     lb.all_gather_rows({0: torch.zeros(2, 3), 1: torch.zeros(2, 3)}, [2, 0])
+    lb.charge("all_gather", [(world - 1) / world * world * 3 * 4 * 4] * world)  # Engine._head_tp
     want = [(r.kind, r.bytes) for r in lb.records if r.device == 0]
     assert [tuple(x) for x in res[0]["ledger"]] == want
     assert [tuple(x) for x in res[1]["ledger"]] == want
