@@ -71,7 +71,14 @@ constexpr int NUM_THREADS = 384;  // 3 warpgroups: softmax 0, softmax 1, produce
 constexpr int Q_TILE_BYTES = QROWS * HD * 2;      // 32 KiB (two 64-wide d chunks)
 constexpr int KV_TILE_BYTES = KT * HD * 2;        // 32 KiB
 constexpr int SMEM_Q = 2 * Q_TILE_BYTES;
-constexpr int SMEM_KV = 2 * 2 * KV_TILE_BYTES;    // 2 stages x (K, V)
+// K ring 2 slots, V ring V_STAGES slots (3 measured no faster than 2: the MMA
+// issuer's V wait shrank from ~400 to ~65 cycles but the period did not move —
+// the tensor core itself, at ~68% of its peak rate, sets it; tools/attn_trace.py)
+#ifndef ATTN_V_STAGES
+#define ATTN_V_STAGES 2
+#endif
+constexpr int K_STAGES = 2, V_STAGES = ATTN_V_STAGES;
+constexpr int SMEM_KV = (K_STAGES + V_STAGES) * KV_TILE_BYTES;
 constexpr int SMEM_BYTES = SMEM_Q + SMEM_KV + 1024 + 256;
 constexpr float kRescaleThreshold = 8.0f;         // log2 units
 
@@ -136,6 +143,21 @@ __device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t smem_addr, uint32_t 
   return d;
 }
 
+#ifdef ATTN_TRACE
+// instrumented build (-DATTN_TRACE): clock64 stamps of CTA (0,0), iterations
+// 0..31: [role][it][event], role 0 = MMA issuer, 1/2 = softmax warpgroup 0/1
+__device__ unsigned long long g_attn_trace[3 * 32 * 8];
+#define TR(role, it, ev)                                                              \
+  do {                                                                                \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && (it) < 32)                              \
+      g_attn_trace[((role) * 32 + (it)) * 8 + (ev)] = clock64();                      \
+  } while (0)
+#else
+#define TR(role, it, ev) \
+  do {                   \
+  } while (0)
+#endif
+
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     prefill_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, const Params p) {
@@ -145,18 +167,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sQ = smem;                 // [tile][dchunk][128 rows][128 B]
-  uint8_t* sKV = smem + SMEM_Q;       // [stage][K | V][dchunk][128 keys][128 B]
+  uint8_t* sKs = smem + SMEM_Q;                            // [K slot][dchunk][128 keys][128 B]
+  uint8_t* sVs = sKs + K_STAGES * KV_TILE_BYTES;           // [V slot][dchunk][128 keys][128 B]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_Q + SMEM_KV);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;   // [2]
-  uint64_t* v_full = bars + 3;   // [2]
-  uint64_t* k_empty = bars + 5;  // [2] K slot free (both tiles' QK done)
-  uint64_t* s_full = bars + 7;   // [2] per Q tile
-  uint64_t* p_full = bars + 9;   // [2] per Q tile
-  uint64_t* o_full = bars + 11;  // [2] per Q tile
-  uint64_t* v_empty = bars + 13; // [2] V slot free (both tiles' PV done)
-  uint64_t* p_half = bars + 15;  // [2] per Q tile: P of keys 0-63 stored (PV may start)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* k_full = bars + 1;   // [K_STAGES]
+  uint64_t* k_empty = bars + 3;  // [K_STAGES] K slot free (both tiles' QK done)
+  uint64_t* s_full = bars + 5;   // [2] per Q tile
+  uint64_t* p_full = bars + 7;   // [2] per Q tile
+  uint64_t* o_full = bars + 9;   // [2] per Q tile
+  uint64_t* p_half = bars + 11;  // [2] per Q tile: P of keys 0-63 stored (PV may start)
+  uint64_t* v_full = bars + 13;  // [V_STAGES]
+  uint64_t* v_empty = bars + 16; // [V_STAGES] V slot free (both tiles' PV done)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int2 wk = p.work[blockIdx.x];
@@ -185,11 +208,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     mbar_init(q_full, 1);
+    for (int s = 0; s < V_STAGES; ++s) {
+      mbar_init(v_full + s, 1);
+      mbar_init(v_empty + s, 1);
+    }
     for (int s = 0; s < 2; ++s) {
       mbar_init(k_full + s, 1);
-      mbar_init(v_full + s, 1);
       mbar_init(k_empty + s, 1);
-      mbar_init(v_empty + s, 1);
       mbar_init(s_full + s, 1);
       mbar_init(p_full + s, 4);  // one arrival per softmax warp
       mbar_init(p_half + s, 4);
@@ -215,9 +240,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                       kvh * G, q_row0 + tok0 + t * toks_per_tile);
       const int32_t* bt = p.block_tables + (int64_t)item * p.bt_stride;
       for (int it = 0; it < n_it; ++it) {
-        const int j = j_begin + it, s = it & 1;
-        uint8_t* sK = sKV + s * 2 * KV_TILE_BYTES;
-        uint8_t* sV = sK + KV_TILE_BYTES;
+        const int j = j_begin + it, s = it & 1, vs = it % V_STAGES;
+        uint8_t* sK = sKs + s * KV_TILE_BYTES;
+        uint8_t* sV = sVs + vs * KV_TILE_BYTES;
         int rows[2];
         for (int h = 0; h < 2; ++h) {
           const int key0 = j * KT + h * 64;
@@ -233,11 +258,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int c = 0; c < 2; ++c)
           for (int h = 0; h < 2; ++h)
             tma_load_2d(sK + c * (KV_TILE_BYTES / 2) + h * 8192, &tmK, k_full + s, c * 64, rows[h]);
-        mbar_wait(v_empty + s, ((it >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(v_full + s, KV_TILE_BYTES);
+        mbar_wait(v_empty + vs, ((it / V_STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(v_full + vs, KV_TILE_BYTES);
         for (int c = 0; c < 2; ++c)
           for (int h = 0; h < 2; ++h)
-            tma_load_2d(sV + c * (KV_TILE_BYTES / 2) + h * 8192, &tmV, v_full + s, c * 64, rows[h]);
+            tma_load_2d(sV + c * (KV_TILE_BYTES / 2) + h * 8192, &tmV, v_full + vs, c * 64, rows[h]);
       }
     }
     __syncwarp();
@@ -250,7 +275,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(q_full, 0);
       auto issue_qk = [&](int t, int it) {  // S_t of this CTA's it-th key tile
         const int s = it & 1;
-        const uint32_t sk = smem_u32(sKV + s * 2 * KV_TILE_BYTES);
+        const uint32_t sk = smem_u32(sKs + s * KV_TILE_BYTES);
         const uint32_t qa = sq + t * Q_TILE_BYTES;
         const uint32_t d_tmem = tmem + t * 128;
 #pragma unroll
@@ -267,10 +292,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       issue_qk(1, 0);
       umma_commit(k_empty + 0);
       for (int it = 0; it < n_it; ++it) {
-        const int s = it & 1;
-        const uint32_t par = (it >> 1) & 1;
-        mbar_wait(v_full + s, par);
-        const uint32_t sv = smem_u32(sKV + s * 2 * KV_TILE_BYTES + KV_TILE_BYTES);
+        const int s = it & 1, vs = it % V_STAGES;
+        TR(0, it, 0);
+        mbar_wait(v_full + vs, (it / V_STAGES) & 1);
+        TR(0, it, 1);
+        const uint32_t sv = smem_u32(sVs + vs * KV_TILE_BYTES);
         const bool more = it + 1 < n_it;
         if (more) mbar_wait(k_full + (s ^ 1), ((it + 1) >> 1) & 1);
         for (int t = 0; t < 2; ++t) {
@@ -280,6 +306,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             mbar_wait((h == 0 ? p_half : p_full) + t, it & 1);
+            TR(0, it, 2 + 2 * t + h);
             tc_fence_after();
 #pragma unroll
             for (int k = h * (KT / 32); k < (h + 1) * (KT / 32); ++k) {
@@ -291,8 +318,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             issue_qk(t, it + 1);
           else
             umma_commit(o_full + t);
+          TR(0, it, 6 + t);
         }
-        umma_commit(v_empty + s);
+        umma_commit(v_empty + vs);
         if (more) umma_commit(k_empty + (s ^ 1));
       }
     }
@@ -314,16 +342,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     float m_run = -INFINITY, l_run = 0.f;
     for (int it = 0; it < n_it; ++it) {
       const int j = j_begin + it;
+      if (quarter == 0 && lane == 0) TR(1 + t, it, 0);
       mbar_wait(s_full + t, it & 1);
+      if (quarter == 0 && lane == 0) TR(1 + t, it, 1);
       tc_fence_after();
       float s[KT];  // raw scores; the softmax scale is folded into one FFMA below
+      {
+        // all four 32-column loads in flight, one wait (not a TMEM round trip each)
+        uint32_t r[KT / 32][32];
 #pragma unroll
-      for (int c = 0; c < KT / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(s_tmem + c * 32, r);
+        for (int c = 0; c < KT / 32; ++c) tmem_ld32(s_tmem + c * 32, r[c]);
         tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(r[e]);
+        for (int c = 0; c < KT / 32; ++c)
+#pragma unroll
+          for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(r[c][e]);
       }
       const int kbase = j * KT;
       if (kbase + KT - 1 > limit) {
@@ -331,9 +364,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int e = 0; e < KT; ++e)
           if (kbase + e > limit) s[e] = -INFINITY;
       }
-      float mx = -INFINITY;
+      // row max as 8 independent FMNMX3 chains (depth 8 + 3) instead of one
+      // 64-deep dependent chain
+      float mxs[8];
 #pragma unroll
-      for (int e = 0; e < KT; ++e) mx = fmaxf(mx, s[e]);
+      for (int i = 0; i < 8; ++i) mxs[i] = fmaxf(s[2 * i], s[2 * i + 1]);
+#pragma unroll
+      for (int e = 16; e < KT; e += 16)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mxs[i] = fmaxf(mxs[i], fmaxf(s[e + 2 * i], s[e + 2 * i + 1]));
+#pragma unroll
+      for (int w = 4; w; w >>= 1)
+#pragma unroll
+        for (int i = 0; i < w; ++i) mxs[i] = fmaxf(mxs[i], mxs[i + w]);
+      const float mx = mxs[0];
+      if (quarter == 0 && lane == 0) TR(1 + t, it, 2);
       const float m_new = fmaxf(m_run, mx * p.scale_log2);
       const bool need = m_new > m_run + kRescaleThreshold;
       float corr = 1.f;
@@ -359,7 +404,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // SFU is not the co-bottleneck with the tensor core) + FADD2 per pair
       const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2);
       const uint64_t nm2 = f2_pack(-m_run, -m_run);
-      uint64_t sum2 = f2_pack(0.f, 0.f);
+      // row sum in 4 independent FADD2 chains (summed at the end)
+      uint64_t sums[4] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
 #pragma unroll
       for (int c = 0; c < KT / 64; ++c) {
         uint32_t pk[32];
@@ -373,7 +419,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint32_t pb;
             asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(pb) : "r"(pack_bf16x2(a, b)));
             const float2 pf = unpack_bf16x2(pb);
-            sum2 = f2_add(sum2, f2_pack(pf.x, pf.y));
+            sums[e & 3] = f2_add(sums[e & 3], f2_pack(pf.x, pf.y));
             pk[e] = pb;
             continue;
           }
@@ -385,7 +431,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             a = fast_exp2(a);
             b = fast_exp2(b);
           }
-          sum2 = f2_add(sum2, f2_pack(a, b));
+          sums[e & 3] = f2_add(sums[e & 3], f2_pack(a, b));
           pk[e] = pack_bf16x2(a, b);
         }
         tmem_st32(s_tmem + c * 32, pk);
@@ -394,8 +440,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(p_half + t);
+          if (quarter == 0 && lane == 0) TR(1 + t, it, 3);
         }
       }
+      const uint64_t sum2 = f2_add(f2_add(sums[0], sums[1]), f2_add(sums[2], sums[3]));
       float sa, sb;
       f2_unpack(sum2, sa, sb);
       l_run += sa + sb;
@@ -403,6 +451,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_before();
       __syncwarp();  // every lane's P stores complete before the warp's single arrival
       if (lane == 0) mbar_arrive(p_full + t);
+      if (quarter == 0 && lane == 0) TR(1 + t, it, 4);
     }
     // ------------------------------------------------------------- epilogue
     mbar_wait(o_full + t, 0);
@@ -588,3 +637,10 @@ int launch_prefill_tc(const void* q, int64_t ldq, int64_t q_rows_total, const vo
 }
 
 }  // namespace sp
+
+#ifdef ATTN_TRACE
+extern "C" int sp_attn_trace_copy(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, sp::attn_tc::g_attn_trace,
+                                   sizeof(unsigned long long) * (n < 768 ? n : 768));
+}
+#endif
