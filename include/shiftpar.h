@@ -114,6 +114,66 @@ int sp_gemm_plan(int M, int N, int K, int epilogue, int sms);
  * (1 outside the split-K regime).  Host-only, deterministic. */
 int sp_gemm_partials(int M, int N, int K);
 
+/* ------------------------------------------------ fused decode layer
+ * One persistent kernel (one CTA per SM) for the projections of a TP (P = 1)
+ * decode pass between two attention calls — the layer loop body of
+ * _forward_tp (parallel_engine.py:359-379) minus the attention itself:
+ *   [leading RMSNorm]  lead_out = norm(x) * lead_gain              (:354)
+ *   proj[i]  (in order)  acc = x_in[rows][k] . w[n][k]^T, then by kind:
+ *     SP_DL_RES_NORM : x += acc (residual, :369/:377); out = norm(x) * gain
+ *                      (:372, or the next layer's :354 / final :390);
+ *                      out == NULL: residual add only
+ *     SP_DL_SWIGLU   : out[:, c] = silu(acc[gate c]) * acc[up c], w rows
+ *                      interleaved [gate 128 | up 128] as SP_EPI_SWIGLU (:376)
+ *     SP_DL_ROPE_KV  : the QKV projection (:359-361): q rotated -> q_out,
+ *                      k rotated / v -> k_pool / v_pool at slot[r] exactly as
+ *                      sp_rope_kv_write lays them out (head_dim 128)
+ * Later projections read rows the earlier ones write (proj[i].x may alias an
+ * earlier out); the kernel orders them with grid barriers on `sync` (2
+ * zero-initialised uint32 per stream; re-armed by the kernel itself, so CUDA
+ * graph replays are safe).  rows <= 64; each output is a fixed ascending-k
+ * sum of stream-K segment partials: deterministic run to run, equal to the
+ * unfused path within f32 summation-order rounding (different K split).
+ * Workspace: sp_decode_layer_ws_bytes(args) bytes of f32 partial slabs. */
+#define SP_DL_RES_NORM 0
+#define SP_DL_SWIGLU 1
+#define SP_DL_ROPE_KV 2
+typedef struct {
+  const void* w;   /* bf16 weight rows [n][k] (K-major), row stride ldw */
+  int64_t ldw;
+  const void* x;   /* bf16 input rows [rows][k], row stride ldx */
+  int64_t ldx;
+  int n, k, kind, pad_;
+  const float* gain; /* RES_NORM: gain of the normed output */
+  void* out;         /* RES_NORM: bf16 [rows][n]; SWIGLU: bf16 [rows][n / 2] */
+  int64_t ldo;
+} sp_dl_proj;
+typedef struct {
+  int rows, hidden;     /* decode rows (tokens) <= 64, model width (% 256, <= 8192) */
+  float* x;             /* f32 residual stream [rows][ldx], updated in place */
+  int64_t ldx;
+  float eps;
+  int n_proj;           /* 0..4 */
+  sp_dl_proj proj[4];
+  const float* lead_gain; /* optional leading RMSNorm of x -> lead_out (bf16, ld_lead) */
+  void* lead_out;
+  int64_t ld_lead;
+  const int32_t* pos;   /* ROPE_KV: positions [rows], cache slots [rows] (< 0: skip) */
+  const int32_t* slot;
+  const float* rope;    /* [pos][64] (cos, sin) pairs; NULL = no rotation */
+  void* q_out;          /* bf16 [rows][ldq] */
+  int64_t ldq;
+  void* k_pool;
+  void* v_pool;
+  int q_heads, kv_heads, block_size, head_dim;
+  void* ws;             /* f32 partial slabs */
+  int64_t ws_bytes;
+  uint32_t* sync;
+} sp_decode_layer_args;
+sp_status sp_decode_layer(const sp_decode_layer_args* args, void* stream);
+/* Workspace bytes sp_decode_layer needs for these projections (host only; -1 = bad args). */
+int64_t sp_decode_layer_ws_bytes(const sp_decode_layer_args* args);
+
 /* ------------------------------------------------ embedding / norms
  * Embedding gather (parallel_engine.py:339-346 TP, :462-469 SP): out[r, :] =
  * f32(table[ids[r], :]) (+ pos_table[pos[r], :] when pos_table != NULL, the

@@ -72,6 +72,28 @@ SIGNATURES = {
     "sp_softmax_rows_f32": (_c_int, [_vp, _i64, _vp, _i64, _c_int, _c_int, _vp]),
 }
 
+
+
+class DlProj(ctypes.Structure):
+    """sp_dl_proj (include/shiftpar.h)."""
+    _fields_ = [("w", _vp), ("ldw", _i64), ("x", _vp), ("ldx", _i64), ("n", _c_int),
+                ("k", _c_int), ("kind", _c_int), ("pad_", _c_int), ("gain", _vp), ("out", _vp),
+                ("ldo", _i64)]
+
+
+class DecodeLayerArgs(ctypes.Structure):
+    """sp_decode_layer_args (include/shiftpar.h)."""
+    _fields_ = [("rows", _c_int), ("hidden", _c_int), ("x", _vp), ("ldx", _i64), ("eps", _f32),
+                ("n_proj", _c_int), ("proj", DlProj * 4), ("lead_gain", _vp), ("lead_out", _vp),
+                ("ld_lead", _i64), ("pos", _vp), ("slot", _vp), ("rope", _vp), ("q_out", _vp),
+                ("ldq", _i64), ("k_pool", _vp), ("v_pool", _vp), ("q_heads", _c_int),
+                ("kv_heads", _c_int), ("block_size", _c_int), ("head_dim", _c_int), ("ws", _vp),
+                ("ws_bytes", _i64), ("sync", _vp)]
+
+
+SIGNATURES["sp_decode_layer"] = (_c_int, [ctypes.POINTER(DecodeLayerArgs), _vp])
+SIGNATURES["sp_decode_layer_ws_bytes"] = (_i64, [ctypes.POINTER(DecodeLayerArgs)])
+
 _lib = None
 
 

@@ -44,6 +44,7 @@ struct Params {
   int n_splits;
   float* ws_o;    // [items][q_heads][splits][HD]
   float* ws_lse;  // [items][q_heads][splits]
+  int kv_stream;  // decode: K/V pages read once per step -> L2 evict-first hint
 };
 
 // physical 16-byte chunk index of logical (row, chunk) in a [rows][HD] bf16 tile
@@ -500,10 +501,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 2) decode_tma_kernel(
         const int row = (page * p.kv_heads + kvh) * p.block_size + key0 % p.block_size;
         uint8_t* st = smem + s * STAGE_BYTES;
         mbar_arrive_expect_tx(full + s, STAGE_BYTES);
-        tma_load_2d(st, &tmK, full + s, 0, row);
-        tma_load_2d(st + TILE_BYTES / 2, &tmK, full + s, 64, row);
-        tma_load_2d(st + TILE_BYTES, &tmV, full + s, 0, row);
-        tma_load_2d(st + TILE_BYTES + TILE_BYTES / 2, &tmV, full + s, 64, row);
+        if (p.kv_stream) {
+          const uint64_t pol = l2_evict_first_policy();
+          tma_load_2d_hint(st, &tmK, full + s, 0, row, pol);
+          tma_load_2d_hint(st + TILE_BYTES / 2, &tmK, full + s, 64, row, pol);
+          tma_load_2d_hint(st + TILE_BYTES, &tmV, full + s, 0, row, pol);
+          tma_load_2d_hint(st + TILE_BYTES + TILE_BYTES / 2, &tmV, full + s, 64, row, pol);
+        } else {
+          tma_load_2d(st, &tmK, full + s, 0, row);
+          tma_load_2d(st + TILE_BYTES / 2, &tmK, full + s, 64, row);
+          tma_load_2d(st + TILE_BYTES, &tmV, full + s, 0, row);
+          tma_load_2d(st + TILE_BYTES + TILE_BYTES / 2, &tmV, full + s, 64, row);
+        }
       }
       if (!waited) pdl_wait();
     }
@@ -785,6 +794,7 @@ extern "C" sp_status sp_attention(const void* q, int64_t ldq, int64_t q_rows, co
     if (int rc = tma_map_bf16(&tk, k_pool, 2, dims, strides, box)) return rc;
     if (int rc = tma_map_bf16(&tv, v_pool, 2, dims, strides, box)) return rc;
     p.n_splits = attn::decode_tma_splits(n_items, kv_heads, max_kv_len);
+    p.kv_stream = l2_hint_enabled() ? 1 : 0;
     p.ws_o = p.ws_lse = nullptr;
     if (p.n_splits > 1) {
       const int64_t need = (int64_t)n_items * q_heads * p.n_splits * (head_dim + 1) * 4;

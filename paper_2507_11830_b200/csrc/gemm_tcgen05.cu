@@ -67,6 +67,7 @@ struct Params {
   float* ws;
   int group_m;  // m-tiles per raster group (A rows of a group stay L2-resident)
   int group_n;  // > 0: n-tiles per raster group instead (B rows stay L2-resident)
+  int w_stream;  // swap-AB: weights are streamed once -> L2 evict-first hint
   // fused all-to-all: column block b = n / peer_width goes to peer b's buffer
   // peer_ptrs[b] at row (m + peer_row_off) — stores cross NVLink directly
   const unsigned long long* peer_ptrs;
@@ -331,6 +332,7 @@ __global__ void __launch_bounds__(NUM_THREADS, Tile<BN_>::MIN_BLOCKS)
       // the activation (A) loads of those stages are issued after it.
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t evict_first = l2_evict_first_policy();
       int n_def = 0;
       int def_stage[STAGES], def_kc[STAGES], def_m[STAGES], def_ko[STAGES];
       bool waited = false;
@@ -615,6 +617,7 @@ __global__ void __launch_bounds__(NUM_THREADS, SwapTile<NT>::CTAS_PER_SM)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t evict_first = l2_evict_first_policy();
       int n_def = 0;
       int def_stage[STAGES], def_kc[STAGES], def_ko[STAGES];
       bool waited = false;
@@ -633,7 +636,13 @@ __global__ void __launch_bounds__(NUM_THREADS, SwapTile<NT>::CTAS_PER_SM)
             ko = k / p.a_kchunk;
             kc = k - ko * p.a_kchunk;
           }
-          tma_load_2d(sw, &tmW, full + stage, k, row0);  // weights: no dependency on the predecessor
+          // weights: no dependency on the predecessor; streamed exactly once per
+          // decode step, so evicted first from L2 (keeps activations, partial
+          // sums and code resident between the step's kernels)
+          if (p.w_stream)
+            tma_load_2d_hint(sw, &tmW, full + stage, k, row0, evict_first);
+          else
+            tma_load_2d(sw, &tmW, full + stage, k, row0);
           if (waited) {
             tma_load_3d(sw + T::W_BYTES, &tmX, full + stage, kc, 0, ko);
           } else {
@@ -857,6 +866,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t evict_first = l2_evict_first_policy();
       int n_def = 0;
       int def_stage[pair::STAGES], def_kc[pair::STAGES], def_m[pair::STAGES], def_ko[pair::STAGES];
       bool waited = false;
@@ -1340,6 +1350,7 @@ static int launch_swap(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   p.peer_stride = peer_stride;
   p.group_m = 1;
   p.group_n = 0;
+  p.w_stream = l2_hint_enabled() ? 1 : 0;
   p.ws = ks > 1 ? ws : nullptr;
   p.ksplit = (int)ks;
   p.kb_per_split = (int)per;

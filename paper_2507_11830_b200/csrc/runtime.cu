@@ -32,6 +32,15 @@ bool pdl_enabled() {
   return on == 1;
 }
 
+bool l2_hint_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SP_L2_HINT");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 int check_launch(const char* what) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();

@@ -337,6 +337,12 @@ class Engine:
         self.cuda_graphs = cuda_graphs
         self._fuse_splitk = os.environ.get("SP_FUSE_SPLITK", "1") != "0"
         self._fuse_rope = os.environ.get("SP_FUSE_ROPE", "1") != "0"
+        # fused decode layer (one persistent kernel per layer, P = 1 TP decode):
+        # opt-in (SP_DECODE_FUSED=1) — measured slower than the kernel chain
+        # ("fused decode layer")
+        self._decode_fused = os.environ.get("SP_DECODE_FUSED", "0") == "1"
+        self._dl_sync = torch.zeros(2, dtype=torch.int32, device=self.device)
+        self._dl_ws: Dict[int, int] = {}
         self._graph_after = max(1, int(os.environ.get("SP_GRAPH_AFTER", "2")))
         self._graphs: Dict[tuple, _GraphEntry] = {}
         self._graph_pool = torch.cuda.graph_pool_handle() if cuda_graphs else None
@@ -740,6 +746,8 @@ class Engine:
 
     # ================================================================= TP
     def _forward_tp(self, meta, batch, meters, span_logits, cut):
+        if self._use_fused_decode(meta, span_logits, cut):
+            return self._forward_tp_fused_decode(meta, batch, meters)
         peer = self._peer
         if (peer is not None and cut is None and two_shot_min_rows() < meta.M <= peer.max_tokens):
             return self._forward_tp_two_shot(meta, batch, meters, span_logits, peer)
@@ -853,6 +861,78 @@ class Engine:
         ops.add_rmsnorm(x_rows, w.final_gain, eps, xf, row_idx=row_idx, rows=n_rows)
         logits = self._head_tp({r: xf for r in g.local_ranks}, n_rows, meters)
         return self._split(logits, meta, span_logits and cut is None)
+
+    def _use_fused_decode(self, meta, span_logits, cut) -> bool:
+        """The fused decode-layer kernel applies: one rank, a decode pass of at
+        most 64 single-token items, SwiGLU, head_dim 128, widths it tiles.
+        Opt-in (SP_DECODE_FUSED=1); SP_GEMM_NO_SPLITK (which pins the one-chain
+        GEMM numerics for the cross-mode bit-identity tests) keeps the unfused path."""
+        cfg = self.config
+        return (self._decode_fused and self.world_size == 1 and cut is None and not span_logits
+                and meta.decode_like and 0 < meta.M <= 64 and cfg.mlp == "swiglu"
+                and cfg.head_dim == 128 and cfg.hidden % 256 == 0 and cfg.hidden <= 8192
+                and cfg.ffn_dim % 128 == 0 and (cfg.n_heads * cfg.head_dim) % 64 == 0
+                and os.environ.get("SP_GEMM_NO_SPLITK") is None)
+
+    def _forward_tp_fused_decode(self, meta, batch, meters):
+        """TP decode at P = 1 with every layer's projections in ONE persistent
+        kernel (ops.decode_layer): per layer [attention] -> [O + residual +
+        norm, gate/up + SwiGLU, down + residual + next norm, next QKV + RoPE +
+        KV write].  Same algorithm as _forward_tp (parallel_engine.py:333-398);
+        the K-split partial sums differ in split points only."""
+        cfg, w = self.config, self.weights
+        M, h, d = meta.M, cfg.hidden, cfg.head_dim
+        hq, hk, f = cfg.n_heads, cfg.kv_heads, cfg.ffn_dim
+        W, hqw, L = w.qkv_width, hq * d, cfg.n_layers
+        dev, eps = self.device, cfg.norm_eps
+        bf = torch.bfloat16
+        x = torch.empty((M, h), dtype=torch.float32, device=dev)
+        ops.embed(meta.toks, w.embed, x, meta.pos, w.pos_table)
+        xn = torch.empty((M, h), dtype=bf, device=dev)
+        xn2 = torch.empty((M, h), dtype=bf, device=dev)
+        xf = torch.empty((M, h), dtype=bf, device=dev)
+        act = torch.empty((M, f), dtype=bf, device=dev)
+        q = torch.empty((M, hqw), dtype=bf, device=dev)
+        o = torch.empty((M, hqw), dtype=bf, device=dev)
+
+        def qkv(layer):
+            return ops.DlProj(w.layers[layer].wqkv, xn, ops.DL_ROPE_KV, n=W, k=h, ldw=h)
+
+        def rope(layer):
+            return dict(pos=meta.pos, slot=meta.slots, rope=w.rope, q_out=q,
+                        k_pool=self.pool.layer_k(0, layer), v_pool=self.pool.layer_v(0, layer),
+                        q_heads=hq, kv_heads=hk, block_size=self.pool.block_size, head_dim=d)
+
+        def body(layer):
+            lw = w.layers[layer]
+            last = layer == L - 1
+            nxt = None if last else w.layers[layer + 1]
+            return [ops.DlProj(lw.wo, o, ops.DL_RES_NORM, n=h, k=hqw, ldw=hq * d,
+                               gain=lw.mlp_gain, out=xn2),
+                    ops.DlProj(lw.wgu, xn2, ops.DL_SWIGLU, n=2 * f, k=h, ldw=h, out=act),
+                    ops.DlProj(lw.wdown, act, ops.DL_RES_NORM, n=h, k=f, ldw=f,
+                               gain=w.final_gain if last else nxt.attn_gain,
+                               out=xf if last else xn)] + ([] if last else [qkv(layer + 1)])
+
+        nb = self._dl_ws.get(M)
+        if nb is None:
+            nb = max(ops.decode_layer_ws_bytes(M, x, body(0)),
+                     ops.decode_layer_ws_bytes(M, x, [qkv(0)]))
+            self._dl_ws[M] = nb
+        ws = torch.empty(-(-nb // 4), dtype=torch.float32, device=dev)
+        self._stage_all(0, batch)
+        ops.decode_layer(M, x, eps, [qkv(0)], ws=ws, sync=self._dl_sync,
+                         lead_gain=w.layers[0].attn_gain, lead_out=xn, rope_args=rope(0),
+                         meter=meters[0])
+        for layer in range(L):
+            self._attend(0, layer, q, o, meta, meters[0])
+            if layer + 1 < L:
+                self._stage_all(layer + 1, batch)
+            ops.decode_layer(M, x, eps, body(layer), ws=ws, sync=self._dl_sync,
+                             rope_args=None if layer + 1 == L else rope(layer + 1),
+                             meter=meters[0])
+        logits = self._head_tp({0: xf}, meta.n, meters)
+        return self._split(logits, meta, False)
 
     def _forward_tp_two_shot(self, meta, batch, meters, span_logits, peer):
         """TP pass for prefill-size M with the two-shot all-reduce over peer

@@ -347,6 +347,85 @@ def rope_kv_write_partials(parts: torch.Tensor, n_parts: int, pos: torch.Tensor,
     _lib.check(rc, "sp_rope_kv_write_partials")
 
 
+DL_RES_NORM = 0
+DL_SWIGLU = 1
+DL_ROPE_KV = 2
+
+
+class DlProj:
+    """One projection of a fused decode layer (sp_dl_proj): acc = x · w^T then
+    ``kind`` (DL_RES_NORM: x_res += acc, out = norm · gain; DL_SWIGLU: out =
+    silu(gate) · up; DL_ROPE_KV: q / paged K,V)."""
+
+    def __init__(self, w: torch.Tensor, x: torch.Tensor, kind: int, *, n: int, k: int,
+                 ldw: int, gain: Optional[torch.Tensor] = None,
+                 out: Optional[torch.Tensor] = None):
+        _need(w, torch.bfloat16, "decode_layer weight")
+        _need(x, torch.bfloat16, "decode_layer input rows")
+        if out is not None:
+            _need(out, torch.bfloat16, "decode_layer output")
+        self.w, self.x, self.kind, self.n, self.k, self.ldw = w, x, kind, n, k, ldw
+        self.gain, self.out = gain, out
+
+
+def _dl_args(rows, x, eps, projs, lead_gain, lead_out, rope_args, ws, sync):
+    a = _lib.DecodeLayerArgs()
+    a.rows, a.hidden = rows, x.shape[1]
+    a.x, a.ldx, a.eps = x.data_ptr(), x.stride(0), eps
+    a.n_proj = len(projs)
+    for i, p in enumerate(projs):
+        d = a.proj[i]
+        d.w, d.ldw, d.x, d.ldx = p.w.data_ptr(), p.ldw, p.x.data_ptr(), p.x.stride(0)
+        d.n, d.k, d.kind = p.n, p.k, p.kind
+        d.gain = _ptr(p.gain)
+        d.out = _ptr(p.out)
+        d.ldo = 0 if p.out is None else p.out.stride(0)
+    if lead_out is not None:
+        a.lead_gain, a.lead_out, a.ld_lead = lead_gain.data_ptr(), lead_out.data_ptr(), lead_out.stride(0)
+    if rope_args is not None:
+        r = rope_args
+        a.pos, a.slot, a.rope = r["pos"].data_ptr(), r["slot"].data_ptr(), _ptr(r["rope"])
+        a.q_out, a.ldq = r["q_out"].data_ptr(), r["q_out"].stride(0)
+        a.k_pool, a.v_pool = r["k_pool"].data_ptr(), r["v_pool"].data_ptr()
+        a.q_heads, a.kv_heads = r["q_heads"], r["kv_heads"]
+        a.block_size, a.head_dim = r["block_size"], r["head_dim"]
+    if ws is not None:
+        a.ws, a.ws_bytes = ws.data_ptr(), ws.numel() * ws.element_size()
+    if sync is not None:
+        a.sync = sync.data_ptr()
+    return a
+
+
+def decode_layer_ws_bytes(rows: int, x: torch.Tensor, projs) -> int:
+    a = _dl_args(rows, x, 0.0, projs, None, None, None, None, None)
+    n = int(_lib.load().sp_decode_layer_ws_bytes(ctypes.byref(a)))
+    if n < 0:
+        raise ContractViolation("decode_layer_ws_bytes: bad arguments")
+    return n
+
+
+def decode_layer(rows: int, x: torch.Tensor, eps: float, projs, *, ws: torch.Tensor,
+                 sync: torch.Tensor, lead_gain: Optional[torch.Tensor] = None,
+                 lead_out: Optional[torch.Tensor] = None, rope_args: Optional[dict] = None,
+                 meter=None) -> None:
+    """sp_decode_layer: the projections of one TP (P = 1) decode layer as ONE
+    persistent kernel (see include/shiftpar.h).  ``sync``: 2 zeroed int32 owned
+    by the caller (the kernel re-arms them)."""
+    _need(x, torch.float32, "decode_layer residual")
+    _need(sync, torch.int32, "decode_layer sync")
+    if meter is not None:
+        for p in projs:
+            meter.add_matmul(rows, p.k, p.n)
+    if rows == 0:
+        return
+    a = _dl_args(rows, x, eps, projs, lead_gain, lead_out, rope_args, ws, sync)
+    flops = sum(2 * rows * p.n * p.k for p in projs)
+    nbytes = sum(p.n * p.k * 2 for p in projs)
+    with _Timed("decode_layer", flops, nbytes):
+        rc = _lib.load().sp_decode_layer(ctypes.byref(a), _stream())
+    _lib.check(rc, "sp_decode_layer")
+
+
 def attn_tile_tokens(q_heads: int, kv_heads: int, head_dim: int, block_size: int) -> int:
     return _lib.load().sp_attn_tile_tokens(q_heads, kv_heads, head_dim, block_size)
 

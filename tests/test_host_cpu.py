@@ -324,3 +324,32 @@ def test_b200_crossover_model():
     assert default_token_threshold(8) == 32
     with pytest.raises(ConfigError):
         default_token_threshold(0)
+
+
+def test_decode_layer_args_layout_matches_header(tmp_path):
+    """The ctypes mirror of sp_decode_layer_args / sp_dl_proj has the C layout
+    (offsets and sizes from gcc on include/shiftpar.h)."""
+    import ctypes
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    fields = [f for f, _ in _lib.DecodeLayerArgs._fields_]
+    pfields = [f for f, _ in _lib.DlProj._fields_]
+    src = tmp_path / "lay.c"
+    src.write_text(
+        '#include <stdio.h>\n#include <stddef.h>\n#include "shiftpar.h"\nint main(void){\n'
+        'printf("%zu\\n", sizeof(sp_decode_layer_args));\n'
+        'printf("%zu\\n", sizeof(sp_dl_proj));\n'
+        + "".join(f'printf("%zu\\n", offsetof(sp_decode_layer_args, {f}));\n' for f in fields)
+        + "".join(f'printf("%zu\\n", offsetof(sp_dl_proj, {f}));\n' for f in pfields)
+        + "return 0;}\n")
+    exe = tmp_path / "lay"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    want = [ctypes.sizeof(_lib.DecodeLayerArgs), ctypes.sizeof(_lib.DlProj)]
+    want += [getattr(_lib.DecodeLayerArgs, f).offset for f in fields]
+    want += [getattr(_lib.DlProj, f).offset for f in pfields]
+    assert got == want
