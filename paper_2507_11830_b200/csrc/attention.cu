@@ -193,8 +193,8 @@ constexpr int PF_KT = 64;
 
 template <int HD>
 __global__ void __launch_bounds__(PF_WARPS * 32) prefill_kernel(Params p) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();  // inputs of this kernel are written by its predecessor
-  pdl_trigger();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw);
   __nv_bfloat16* sK = sQ + PF_ROWS * HD;        // [2][KT][HD]
@@ -291,8 +291,8 @@ constexpr int DC_KT = 32;
 
 template <int HD>
 __global__ void __launch_bounds__(DC_WARPS * 32) decode_kernel(Params p) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();  // inputs of this kernel are written by its predecessor
-  pdl_trigger();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(smem_raw) + warp * (4 * DC_KT * HD);
@@ -404,8 +404,8 @@ __global__ void __launch_bounds__(DC_WARPS * 32) decode_kernel(Params p) {
 }
 
 __global__ void combine_kernel(Params p, int head_dim) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();  // inputs of this kernel are written by its predecessor
-  pdl_trigger();
   const int item = blockIdx.x, qh = blockIdx.y;
   const int64_t base = ((int64_t)item * p.q_heads + qh) * p.n_splits;
   float mx = -INFINITY;

@@ -161,8 +161,8 @@ __device__ unsigned long long g_attn_trace[3 * 32 * 8];
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     prefill_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, const Params p) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();  // inputs of this kernel are written by its predecessor
-  pdl_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -508,8 +508,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // rows x 128 d (thread: one row, 16 d); entries of `combine` are (item, t0,
 // first split, n splits).  Splits are merged in ascending key order.
 __global__ void prefill_combine_kernel(const int4* __restrict__ combine, const Params p) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();
-  pdl_trigger();
   const int4 cb = combine[blockIdx.x];
   const int kvh = blockIdx.y;
   const int prow = blockIdx.z * 32 + (threadIdx.x >> 3);

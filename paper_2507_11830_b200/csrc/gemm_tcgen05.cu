@@ -1050,8 +1050,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 // split-K reduction: v = sum_s ws[s] in ascending s (deterministic), then the
 // epilogue; one thread = 8 consecutive output columns of one row.
 __global__ void splitk_reduce_kernel(const Params p) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();  // inputs of this kernel are written by its predecessor
-  pdl_trigger();
   const int n_out = p.epi == SP_EPI_SWIGLU ? p.N / 2 : p.N;
   const int64_t per_row = n_out / 8;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

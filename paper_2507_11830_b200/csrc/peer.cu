@@ -19,8 +19,8 @@ namespace sp {
 __global__ void peer_scatter_kernel(const uint4* __restrict__ src, int64_t lds_v, int rows_total,
                                     int peers, int my_rank, int width_v,
                                     const unsigned long long* __restrict__ dst_ptrs) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();
-  pdl_trigger();
   const int base = rows_total / peers, rem = rows_total % peers;
   const int64_t n = (int64_t)rows_total * width_v;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -46,8 +46,8 @@ __global__ void peer_scatter_kernel(const uint4* __restrict__ src, int64_t lds_v
 
 __global__ void peer_signal_kernel(const unsigned long long* __restrict__ flag_ptrs, int peers,
                                    int my_rank) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();
-  pdl_trigger();
   if (threadIdx.x < (unsigned)peers) {
     int* f = reinterpret_cast<int*>(flag_ptrs[threadIdx.x]) + my_rank;
     asm volatile("fence.acq_rel.sys;" ::: "memory");
@@ -56,8 +56,8 @@ __global__ void peer_signal_kernel(const unsigned long long* __restrict__ flag_p
 }
 
 __global__ void peer_wait_kernel(int* flags, int peers) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();
-  pdl_trigger();
   if (threadIdx.x < (unsigned)peers) {
     int v = 0;
     do {
@@ -80,8 +80,8 @@ __global__ void peer_allreduce_norm_kernel(const unsigned long long* __restrict_
                                            const float* __restrict__ gain, float eps,
                                            __nv_bfloat16* __restrict__ out, int64_t ldo,
                                            int hidden) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();
-  pdl_trigger();
   const int r = blockIdx.x;
   float* xr = x + (int64_t)r * ldx;
   float v[VEC * 4];
@@ -158,8 +158,8 @@ __global__ void peer_reduce_scatter_norm_kernel(const unsigned long long* __rest
                                                 float eps,
                                                 const unsigned long long* __restrict__ xn_ptrs,
                                                 int64_t ldo, int hidden) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();
-  pdl_trigger();
   const int r = row_lo + blockIdx.x;
   float* xr = x + (int64_t)r * ldx;
   float v[VEC * 4];

@@ -52,8 +52,8 @@ int check_launch(const char* what) {
 __global__ void embed_kernel(const int32_t* __restrict__ ids, const __nv_bfloat16* __restrict__ table,
                              const int32_t* __restrict__ pos, const float* __restrict__ pos_table,
                              float* __restrict__ out, int hidden) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();  // inputs of this kernel are written by its predecessor
-  pdl_trigger();
   const int r = blockIdx.x;
   const int64_t tok = ids[r];
   const __nv_bfloat16* src = table + tok * hidden;
@@ -88,8 +88,8 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, int64_t ldx, const flo
     g[i] = out && c < hidden ? *reinterpret_cast<const float4*>(gain + c)
                              : make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();  // inputs of this kernel are written by its predecessor
-  pdl_trigger();
   constexpr int BATCH = VEC == 1 ? 12 : 4;  // partial loads in flight together
   const int r = blockIdx.x;
   const int64_t src_row = row_idx ? row_idx[r] : r;
@@ -184,8 +184,8 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, const floa
                                int64_t ldq, __nv_bfloat16* __restrict__ k_pool,
                                __nv_bfloat16* __restrict__ v_pool, int rows, int q_heads,
                                int kv_heads, int head_dim, int block_size) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();  // inputs of this kernel are written by its predecessor
-  pdl_trigger();
   const int heads = q_heads + 2 * kv_heads;
   const int half = head_dim >> 1;
   const int tpg = half / 8;  // threads per (token, head) when vectorised
@@ -235,8 +235,8 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, const floa
 // ------------------------------------------------------ a2a pack/unpack
 __global__ void pack_kernel(const uint4* __restrict__ src, int64_t lds_v, uint4* __restrict__ dst,
                             int rows, int peers, int width_v) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();  // inputs of this kernel are written by its predecessor
-  pdl_trigger();
   const int64_t total = (int64_t)rows * peers * width_v;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -249,8 +249,8 @@ __global__ void pack_kernel(const uint4* __restrict__ src, int64_t lds_v, uint4*
 
 __global__ void unpack_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int64_t ldd_v,
                               int rows, int peers, int width_v) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();  // inputs of this kernel are written by its predecessor
-  pdl_trigger();
   const int64_t total = (int64_t)rows * peers * width_v;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -264,8 +264,8 @@ __global__ void unpack_kernel(const uint4* __restrict__ src, uint4* __restrict__
 // ------------------------------------------------------------ small ops
 __global__ void add_f32_kernel(const float4* __restrict__ a, const float4* __restrict__ b,
                                float4* __restrict__ d, int64_t n4) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();  // inputs of this kernel are written by its predecessor
-  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
     float4 x = a[i], y = b[i];
@@ -274,16 +274,16 @@ __global__ void add_f32_kernel(const float4* __restrict__ a, const float4* __res
 }
 
 __global__ void add_f32_tail_kernel(const float* a, const float* b, float* d, int64_t lo, int64_t n) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();  // inputs of this kernel are written by its predecessor
-  pdl_trigger();
   int64_t i = lo + threadIdx.x;
   if (i < n) d[i] = a[i] + b[i];
 }
 
 __global__ void argmax_kernel(const float* __restrict__ logits, int64_t ld, int vocab,
                               int32_t* __restrict__ idx, float* __restrict__ val) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();  // inputs of this kernel are written by its predecessor
-  pdl_trigger();
   const float* row = logits + (int64_t)blockIdx.x * ld;
   float best = -INFINITY;
   int bi = 0x7fffffff;
@@ -333,8 +333,8 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int64_t ld, int 
 __global__ void gather_rows_kernel(const float* __restrict__ src, int64_t lds,
                                    const int32_t* __restrict__ idx, float* __restrict__ dst,
                                    int64_t ldd, int width) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();  // inputs of this kernel are written by its predecessor
-  pdl_trigger();
   const float* s = src + (int64_t)idx[blockIdx.x] * lds;
   float* d = dst + (int64_t)blockIdx.x * ldd;
   for (int c = threadIdx.x; c < width; c += blockDim.x) d[c] = s[c];
@@ -515,8 +515,8 @@ __global__ void rms_norm_f32_kernel(const float* __restrict__ x, int64_t ldx,
                                     const float* __restrict__ gain, float eps,
                                     float* __restrict__ out, int64_t ldo, int hidden) {
   __shared__ float red[32];
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();
-  pdl_trigger();
   const float* row = x + (int64_t)blockIdx.x * ldx;
   float s = 0.f;
   for (int c = threadIdx.x; c < hidden; c += blockDim.x) s += row[c] * row[c];
@@ -538,8 +538,8 @@ __global__ void rms_norm_f32_kernel(const float* __restrict__ x, int64_t ldx,
 
 __global__ void gelu_f32_kernel(const float* __restrict__ x, float* __restrict__ out, int64_t n) {
   const float c = 0.7978845608028654f, k = 0.044715f;  // sqrt(2/pi), tanh-form GeLU
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();
-  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float v = x[i];
@@ -550,8 +550,8 @@ __global__ void gelu_f32_kernel(const float* __restrict__ x, float* __restrict__
 __global__ void softmax_rows_f32_kernel(const float* __restrict__ x, int64_t ldx,
                                         float* __restrict__ out, int64_t ldo, int width) {
   __shared__ float red[32];
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();
-  pdl_trigger();
   const float* row = x + (int64_t)blockIdx.x * ldx;
   float* o = out + (int64_t)blockIdx.x * ldo;
   const int w = blockDim.x >> 5, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -609,8 +609,8 @@ extern "C" sp_status sp_softmax_rows_f32(const float* x, int64_t ldx, float* out
 
 __global__ void add_f64_kernel(const double* __restrict__ a, const double* __restrict__ b,
                                double* __restrict__ d, int64_t n) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();
-  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     d[i] = a[i] + b[i];
@@ -628,8 +628,8 @@ extern "C" sp_status sp_add_f64(const double* a, const double* b, double* dst, i
 __global__ void gather_rows_u16_kernel(const uint16_t* __restrict__ src, int64_t lds,
                                        const int32_t* __restrict__ idx, uint16_t* __restrict__ dst,
                                        int64_t ldd, int width) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();
-  pdl_trigger();
   const uint16_t* s = src + (int64_t)idx[blockIdx.x] * lds;
   uint16_t* d = dst + (int64_t)blockIdx.x * ldd;
   for (int c = threadIdx.x; c < width; c += blockDim.x) d[c] = s[c];
