@@ -1285,10 +1285,16 @@ static int64_t swap_splits(int N, int K, int sms) {
   return cdiv(k_blocks, per);
 }
 
-// the swap-AB (decode) regime applies: one 128-row M tile that cannot cover the SMs
+// the swap-AB (decode) regime applies: one 128-row M tile that cannot cover the SMs.
+// Wide projections (more 256-row weight tiles than a quarter of the SMs) only up
+// to 64 tokens: there the 1-CTA 128x256 tiles stream faster than the swap-AB
+// variants for 65..256 tokens (tools/swap_probe.py, graph-replayed, gate/up
+// N = 28672 K = 4096 at M = 96 / 128 / 256: 42.2 / 42.6 / 55.2 us tiled vs
+// 46.6 / 48.6 / 62.8 swap-AB; at M <= 64 swap-AB wins, 40.3-41.1 vs 43.0-43.3).
 static bool swap_regime(int M, int N, int sms) {
   using namespace sp::gemm;
-  return M <= 256 && cdiv(N, 256) < sms && N % 32 == 0 &&
+  const int64_t n_super = cdiv(N, 256);
+  return M <= 256 && n_super < sms && N % 32 == 0 && (M <= 64 || n_super <= sms / 4) &&
          getenv("SP_GEMM_NO_SPLITK") == nullptr;
 }
 

@@ -46,12 +46,16 @@ class GemmModel:
     tools/tau_sweep.py (profiles/r02_tau_sweep.json; 8B shapes, P = 2/4/8,
     M = 1..4096, graph-replayed): every GEMM costs max(compute, weight
     streaming) plus a fixed, non-overlapped ~9 us; the swap-AB regime
-    (M <= 256 token rows, padded to 32) computes at ~800 TFLOP/s, the
-    128-row tiles above it at ~1400."""
+    (M <= 256 token rows, padded to 32; for projections wider than
+    swap_wide_tiles 256-row weight tiles only up to swap_wide_max_rows, as
+    gemm_tcgen05.cu:swap_regime) computes at ~800 TFLOP/s, the 128-row tiles
+    above it at ~1400."""
 
     tflops: float = 1400.0         # 128/256-row tcgen05 tiles (M > swap_max_rows)
     swap_tflops: float = 800.0     # swap-AB regime
     swap_max_rows: int = 256
+    swap_wide_max_rows: int = 64   # wide projections leave swap-AB above this
+    swap_wide_tiles: int = 37      # "wide": more 256-row weight tiles than sms / 4
     hbm_gbs: float = 6454.6        # MEASURED_PEAKS.json copy bandwidth
     stream_eff: float = 1.0        # weight streaming, fraction of hbm_gbs
     launch_us: float = 9.0         # per-GEMM fixed cost (launch, fill, drain, tail)
@@ -64,7 +68,8 @@ B200_GEMM = GemmModel()
 def _gemm_us(rows: int, n: int, k: int, g: GemmModel) -> float:
     if rows <= 0:
         return 0.0
-    if rows <= g.swap_max_rows:
+    wide = -(-n // 256) > g.swap_wide_tiles
+    if rows <= (g.swap_wide_max_rows if wide else g.swap_max_rows):
         pad, tf = -(-rows // 32) * 32, g.swap_tflops
     else:
         pad, tf = -(-rows // 128) * 128, g.tflops
