@@ -254,6 +254,25 @@ sp_status sp_attention_prefill_split(const void* q, int64_t ldq, int64_t q_rows,
                                      int kv_heads, int head_dim, int block_size, void* ws,
                                      int64_t ws_bytes, void* stream);
 int64_t sp_attn_workspace_bytes(int n_items, int q_heads, int head_dim, int max_kv_len);
+/* Decode attention (one query row per item, cu_q[item] = its row) fed by the
+ * QKV projection's K-split partials instead of a rotated Q: replaces the pair
+ * kv_cache.append (kv_cache.py:99-122, with RoPE) + attend_cached
+ * (tensor_core.py:135-176) of one decode layer (parallel_engine.py:359-368).
+ * parts: [n_parts][parts_rows][ld_qkv] f32, ld_qkv = (q_heads + 2 kv_heads)
+ * * 128, columns [q heads | k heads | v heads].  The kernel sums the partials
+ * in ascending order, rounds to bf16, rotates q and k (rope_table as in
+ * sp_rope_kv_write; NULL = none), writes the row's K/V into the pools at
+ * slot[row] and attends with its Q — bit-identical to
+ * sp_rope_kv_write_partials followed by sp_attention.  head_dim 128,
+ * block_size % 64 == 0; ws as for sp_attention. */
+sp_status sp_attention_decode_qkv(const float* parts, int n_parts, int64_t ld_qkv, int parts_rows,
+                                  const int32_t* pos, const int32_t* slot, const float* rope_table,
+                                  void* k_pool, void* v_pool, int64_t pool_blocks,
+                                  const int32_t* block_tables, int64_t bt_stride,
+                                  const int32_t* cu_q, const int32_t* kv_len, int n_items,
+                                  int max_kv_len, void* out, int64_t ldo, int q_heads,
+                                  int kv_heads, int block_size, void* ws, int64_t ws_bytes,
+                                  void* stream);
 /* Tokens per prefill work tile (host schedule).  head_dim 128 with pages of a
  * multiple of 64 keys selects the tcgen05/TMEM kernel (2 x 128 packed rows
  * per CTA); other shapes use the mma.sync kernel (64 packed rows). */

@@ -59,6 +59,9 @@ SIGNATURES = {
                               _vp, _c_int, _c_int, _c_int, _vp, _i64, _c_int, _c_int, _c_int,
                               _c_int, _vp, _i64, _vp]),
     "sp_attn_workspace_bytes": (_i64, [_c_int, _c_int, _c_int, _c_int]),
+    "sp_attention_decode_qkv": (_c_int, [_vp, _c_int, _i64, _c_int, _vp, _vp, _vp, _vp, _vp, _i64,
+                                         _vp, _i64, _vp, _vp, _c_int, _c_int, _vp, _i64, _c_int,
+                                         _c_int, _c_int, _vp, _i64, _vp]),
     "sp_attn_tile_tokens": (_c_int, [_c_int, _c_int, _c_int, _c_int]),
     "sp_a2a_pack": (_c_int, [_vp, _i64, _vp, _c_int, _c_int, _c_int, _vp]),
     "sp_a2a_unpack": (_c_int, [_vp, _vp, _i64, _c_int, _c_int, _c_int, _vp]),

@@ -16,6 +16,8 @@
 #include <cstdlib>
 
 #include "../../include/shiftpar.h"
+#include <cstring>
+
 #include "common.cuh"
 
 namespace sp {
@@ -45,6 +47,18 @@ struct Params {
   float* ws_o;    // [items][q_heads][splits][HD]
   float* ws_lse;  // [items][q_heads][splits]
   int kv_stream;  // decode: K/V pages read once per step -> L2 evict-first hint
+  // TMA decode with the QKV projection left as K-split partials
+  // ([n_parts][rows][ld_qkv] f32, columns [q heads | k heads | v heads] x 128):
+  // the kernel sums them (ascending), rounds to bf16 and applies RoPE exactly as
+  // rope_kv_kernel does, builds its Q in shared memory, and the CTA holding the
+  // new token's page writes that token's K/V into the pool before its producer
+  // loads the page.  NULL: Q is read from q (written by the RoPE kernel).
+  const float* qkv_parts;
+  int n_parts, parts_rows;
+  int64_t ld_qkv;
+  const int32_t* rope_pos;
+  const int32_t* rope_slot;
+  const float* rope_table;
 };
 
 // physical 16-byte chunk index of logical (row, chunk) in a [rows][HD] bf16 tile
@@ -442,6 +456,77 @@ constexpr int STAGE_BYTES = 2 * TILE_BYTES;
 constexpr int SMEM_Q = 16 * HD * 2;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + SMEM_Q + 1024 + 256;
 
+__device__ __forceinline__ void fence_proxy_async_global_() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Q rows of this CTA's G heads (and, for the new token's CTA, its K and V) from
+// the QKV K-split partials: ascending sum, bf16 rounding, RoPE with
+// rope_rotate — the arithmetic of rope_kv_kernel (qkv_chunk) bit for bit.
+// Q goes to the swizzled sQ tile (rows >= G zero), K/V to the pool at the slot.
+__device__ __forceinline__ void build_q_kv(const Params& p, __nv_bfloat16* sQ, int item, int kvh,
+                                           bool kv_writer, int tid) {
+  const int G = p.group;
+  const int row = p.cu_q[item];
+  const int pos = p.rope_pos[row];
+  const int slot = kv_writer ? p.rope_slot[row] : -1;
+  // rows G..15 of the m16 Q tile are padding: zero them
+  for (int i = tid; i < (16 - G) * (HD / 8); i += NCONS * 32) {
+    const int r = G + i / (HD / 8), c = i % (HD / 8);
+    *reinterpret_cast<uint4*>(sQ + r * HD + c * 8) = make_uint4(0, 0, 0, 0);
+  }
+  const int heads = G + (slot >= 0 ? 2 : 0);
+  for (int it = tid; it < heads * 16; it += NCONS * 32) {
+    const int hh = it >> 4, i0 = (it & 15) * 4;
+    int col_head;
+    bool rotate = p.rope_table != nullptr;
+    if (hh < G) {
+      col_head = kvh * G + hh;
+    } else if (hh == G) {
+      col_head = p.q_heads + kvh;
+    } else {
+      col_head = p.q_heads + p.kv_heads + kvh;
+      rotate = false;
+    }
+    const float* src = p.qkv_parts + (int64_t)row * p.ld_qkv + (int64_t)col_head * HD + i0;
+    const int64_t pstride = (int64_t)p.parts_rows * p.ld_qkv;
+    float a[4] = {0.f, 0.f, 0.f, 0.f}, b[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int sidx = 0; sidx < p.n_parts; ++sidx) {
+      const float4 x = *reinterpret_cast<const float4*>(src + sidx * pstride);
+      const float4 y = *reinterpret_cast<const float4*>(src + sidx * pstride + 64);
+      a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+      b[0] += y.x; b[1] += y.y; b[2] += y.z; b[3] += y.w;
+    }
+    uint32_t ua[2] = {pack_bf16x2(a[0], a[1]), pack_bf16x2(a[2], a[3])};
+    uint32_t ub[2] = {pack_bf16x2(b[0], b[1]), pack_bf16x2(b[2], b[3])};
+    if (rotate) {
+      const float4* cs = reinterpret_cast<const float4*>(p.rope_table + ((int64_t)pos * (HD / 2) + i0) * 2);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const float4 c2 = cs[q];
+        const float2 fa = unpack_bf16x2(ua[q]);
+        const float2 fb = unpack_bf16x2(ub[q]);
+        float na0, nb0, na1, nb1;
+        rope_rotate(fa.x, fb.x, c2.x, c2.y, na0, nb0);
+        rope_rotate(fa.y, fb.y, c2.z, c2.w, na1, nb1);
+        ua[q] = pack_bf16x2(na0, na1);
+        ub[q] = pack_bf16x2(nb0, nb1);
+      }
+    }
+    if (hh < G) {
+      __nv_bfloat16* rowp = sQ + hh * HD;
+      *reinterpret_cast<uint2*>(rowp + swz<HD>(hh, i0 >> 3) * 8 + (i0 & 7)) = make_uint2(ua[0], ua[1]);
+      *reinterpret_cast<uint2*>(rowp + swz<HD>(hh, (i0 + 64) >> 3) * 8 + (i0 & 7)) = make_uint2(ub[0], ub[1]);
+    } else {
+      __nv_bfloat16* pool = const_cast<__nv_bfloat16*>(hh == G ? p.k_pool : p.v_pool);
+      const int64_t blk = slot / p.block_size, off = slot % p.block_size;
+      __nv_bfloat16* dst = pool + ((blk * p.kv_heads + kvh) * p.block_size + off) * HD;
+      *reinterpret_cast<uint2*>(dst + i0) = make_uint2(ua[0], ua[1]);
+      *reinterpret_cast<uint2*>(dst + 64 + i0) = make_uint2(ub[0], ub[1]);
+    }
+  }
+}
+
 // (key, 16-byte chunk) inside a [2 d-chunks][64 keys][128 B] swizzled slice
 __device__ __forceinline__ uint32_t kv_addr(uint32_t base, int key, int c16) {
   return base + (c16 >> 3) * (TILE_BYTES / 2) + key * 128 + ((((c16 & 7) ^ (key & 7))) << 4);
@@ -461,6 +546,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2) decode_tma_kernel(
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem + STAGES * STAGE_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + SMEM_Q);
   uint64_t* empty = full + STAGES;
+  uint64_t* kv_ready = empty + STAGES;  // fused QKV: the new token's K/V are in the pool
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int item = blockIdx.x, kvh = blockIdx.y, split = blockIdx.z;
   const int G = p.group;
@@ -479,9 +565,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 2) decode_tma_kernel(
       mbar_init(full + s, 1);
       mbar_init(empty + s, NCONS);
     }
+    mbar_init(kv_ready, 1);
     fence_barrier_init();
   }
   __syncthreads();  // barriers initialised
+  // fused QKV: this CTA holds the new token's page (and writes its K/V)
+  const bool kv_writer = p.qkv_parts != nullptr && t_begin <= n_tiles - 1 && n_tiles - 1 < t_end;
 
   float o[HD / 8][4];
   float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
@@ -494,6 +583,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2) decode_tma_kernel(
           pdl_wait();
           waited = true;
         }
+        if (kv_writer && t == old_tiles) mbar_wait(kv_ready, 0);  // written by the consumer warps
         const int s = i % STAGES;
         mbar_wait(empty + s, ((i / STAGES) & 1) ^ 1);
         const int key0 = t * PAGE;
@@ -518,8 +608,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 2) decode_tma_kernel(
     }
     __syncwarp();
   } else {
-    pdl_wait();  // Q is written by the predecessor
-    {
+    pdl_wait();  // Q (or the QKV partials) is written by the predecessor
+    if (p.qkv_parts != nullptr) {
+      build_q_kv(p, sQ, item, kvh, kv_writer, tid);
+      if (kv_writer) fence_proxy_async_global_();  // pool writes -> this CTA's TMA loads
+      asm volatile("bar.sync 1, %0;" ::"n"(NCONS * 32) : "memory");  // consumer warps only
+      if (kv_writer && tid == 0) mbar_arrive(kv_ready);
+    } else {
       constexpr int NCH = HD / 8;
       for (int i = tid; i < 16 * NCH; i += NCONS * 32) {
         const int r = i / NCH, c = i % NCH;
@@ -708,6 +803,44 @@ extern "C" int64_t sp_attn_workspace_bytes(int n_items, int q_heads, int head_di
   return (int64_t)n_items * q_heads * splits * (head_dim + 1) * 4;
 }
 
+static sp_status launch_decode_tma(attn::Params& p, const void* k_pool, const void* v_pool,
+                                   int64_t pool_blocks, int n_items, int q_heads, int kv_heads,
+                                   int head_dim, int block_size, int max_kv_len, void* ws,
+                                   int64_t ws_bytes, cudaStream_t st) {
+  CUtensorMap tk, tv;
+  uint64_t dims[2] = {128, (uint64_t)(pool_blocks * (int64_t)kv_heads * block_size)};
+  uint64_t strides[1] = {128 * 2};
+  uint32_t box[2] = {64, attn::dec::PAGE};
+  if (int rc = tma_map_bf16(&tk, k_pool, 2, dims, strides, box)) return rc;
+  if (int rc = tma_map_bf16(&tv, v_pool, 2, dims, strides, box)) return rc;
+  p.n_splits = attn::decode_tma_splits(n_items, kv_heads, max_kv_len);
+  p.kv_stream = l2_hint_enabled() ? 1 : 0;
+  p.ws_o = p.ws_lse = nullptr;
+  if (p.n_splits > 1) {
+    const int64_t need = (int64_t)n_items * q_heads * p.n_splits * (head_dim + 1) * 4;
+    if (!ws || ws_bytes < need) {
+      p.n_splits = 1;
+    } else {
+      p.ws_o = static_cast<float*>(ws);
+      p.ws_lse = p.ws_o + (int64_t)n_items * q_heads * p.n_splits * head_dim;
+    }
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn::dec::decode_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         attn::dec::SMEM_BYTES);
+    attr = true;
+  }
+  launch_k(attn::dec::decode_tma_kernel, dim3(n_items, kv_heads, p.n_splits), attn::dec::NUM_THREADS,
+           attn::dec::SMEM_BYTES, st, tk, tv, p);
+  if (int rc = check_launch("attn_decode_tma_kernel")) return rc;
+  if (p.n_splits > 1) {
+    launch_k(attn::combine_kernel, dim3(n_items, q_heads), head_dim, 0, st, p, head_dim);
+    return check_launch("attn_combine_kernel");
+  }
+  return kOk;
+}
+
 extern "C" sp_status sp_attention_prefill_split(
     const void* q, int64_t ldq, int64_t q_rows, const void* k_pool, const void* v_pool,
     int64_t pool_blocks, const int32_t* block_tables, int64_t bt_stride, const int32_t* cu_q,
@@ -765,6 +898,8 @@ extern "C" sp_status sp_attention(const void* q, int64_t ldq, int64_t q_rows, co
   p.n_splits = 1;
   p.ws_o = nullptr;
   p.ws_lse = nullptr;
+  p.kv_stream = 0;
+  p.qkv_parts = nullptr;
   if (n_work == 0) {
     p.n_splits = attn::decode_splits(n_items, kv_heads, max_kv_len);
     if (p.n_splits > 1) {
@@ -786,43 +921,61 @@ extern "C" sp_status sp_attention(const void* q, int64_t ldq, int64_t q_rows, co
                              cu_q, first_pos, kv_len, work, n_work, out, ldo, q_heads, kv_heads,
                              block_size, st);
   }
-  if (n_work == 0 && head_dim == 128 && block_size % attn::dec::PAGE == 0 && pool_blocks > 0) {
-    CUtensorMap tk, tv;
-    uint64_t dims[2] = {128, (uint64_t)(pool_blocks * (int64_t)kv_heads * block_size)};
-    uint64_t strides[1] = {128 * 2};
-    uint32_t box[2] = {64, attn::dec::PAGE};
-    if (int rc = tma_map_bf16(&tk, k_pool, 2, dims, strides, box)) return rc;
-    if (int rc = tma_map_bf16(&tv, v_pool, 2, dims, strides, box)) return rc;
-    p.n_splits = attn::decode_tma_splits(n_items, kv_heads, max_kv_len);
-    p.kv_stream = l2_hint_enabled() ? 1 : 0;
-    p.ws_o = p.ws_lse = nullptr;
-    if (p.n_splits > 1) {
-      const int64_t need = (int64_t)n_items * q_heads * p.n_splits * (head_dim + 1) * 4;
-      if (!ws || ws_bytes < need) {
-        p.n_splits = 1;
-      } else {
-        p.ws_o = static_cast<float*>(ws);
-        p.ws_lse = p.ws_o + (int64_t)n_items * q_heads * p.n_splits * head_dim;
-      }
-    }
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(attn::dec::decode_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           attn::dec::SMEM_BYTES);
-      attr = true;
-    }
-    launch_k(attn::dec::decode_tma_kernel, dim3(n_items, kv_heads, p.n_splits), attn::dec::NUM_THREADS, attn::dec::SMEM_BYTES, st, tk, tv, p);
-    if (int rc = check_launch("attn_decode_tma_kernel")) return rc;
-    if (p.n_splits > 1) {
-      launch_k(attn::combine_kernel, dim3(n_items, q_heads), head_dim, 0, st, p, head_dim);
-      return check_launch("attn_combine_kernel");
-    }
-    return kOk;
-  }
+  if (n_work == 0 && head_dim == 128 && block_size % attn::dec::PAGE == 0 && pool_blocks > 0)
+    return launch_decode_tma(p, k_pool, v_pool, pool_blocks, n_items, q_heads, kv_heads, head_dim,
+                             block_size, max_kv_len, ws, ws_bytes, st);
   switch (head_dim) {
     case 32: return attn::launch<32>(p, n_items, n_work, st);
     case 64: return attn::launch<64>(p, n_items, n_work, st);
     case 128: return attn::launch<128>(p, n_items, n_work, st);
     default: return fail(kUnsupported, "attention: head_dim must be 32, 64 or 128");
   }
+}
+
+// Decode attention whose Q, and the new token's K/V, come from the QKV
+// projection's K-split partials (the RoPE + KV-write kernel fused into the
+// attention kernel): see attn::Params::qkv_parts.  One row per item
+// (cu_q[item] = its row); head_dim 128, block_size % 64 == 0.  Bit-identical
+// to sp_rope_kv_write_partials followed by sp_attention.
+extern "C" sp_status sp_attention_decode_qkv(
+    const float* parts, int n_parts, int64_t ld_qkv, int parts_rows, const int32_t* pos,
+    const int32_t* slot, const float* rope_table, void* k_pool, void* v_pool, int64_t pool_blocks,
+    const int32_t* block_tables, int64_t bt_stride, const int32_t* cu_q, const int32_t* kv_len,
+    int n_items, int max_kv_len, void* out, int64_t ldo, int q_heads, int kv_heads,
+    int block_size, void* ws, int64_t ws_bytes, void* stream) {
+  if (n_items < 0 || n_parts < 1 || parts_rows < n_items) return fail(kInvalid, "attention_decode_qkv: bad sizes");
+  if (n_items == 0) return kOk;
+  if (!parts || !pos || !slot || !k_pool || !v_pool || !block_tables || !cu_q || !kv_len || !out)
+    return fail(kInvalid, "attention_decode_qkv: null pointer");
+  if (kv_heads <= 0 || q_heads % kv_heads) return fail(kInvalid, "attention: q_heads % kv_heads != 0");
+  const int G = q_heads / kv_heads;
+  if (G > 16) return fail(kUnsupported, "attention: GQA group > 16");
+  if (block_size <= 0 || block_size % attn::dec::PAGE || pool_blocks <= 0)
+    return fail(kUnsupported, "attention_decode_qkv: block_size must be a multiple of 64");
+  if (ld_qkv != (int64_t)(q_heads + 2 * kv_heads) * 128 || ldo % 2)
+    return fail(kInvalid, "attention_decode_qkv: ld_qkv must be (q_heads + 2 kv_heads) * 128");
+  attn::Params p;
+  memset(&p, 0, sizeof(p));
+  p.k_pool = static_cast<const __nv_bfloat16*>(k_pool);
+  p.v_pool = static_cast<const __nv_bfloat16*>(v_pool);
+  p.block_tables = block_tables;
+  p.bt_stride = bt_stride;
+  p.cu_q = cu_q;
+  p.kv_len = kv_len;
+  p.out = static_cast<__nv_bfloat16*>(out);
+  p.ldo = ldo;
+  p.q_heads = q_heads;
+  p.kv_heads = kv_heads;
+  p.group = G;
+  p.block_size = block_size;
+  p.scale_log2 = attn::kLog2e / sqrtf(128.f);
+  p.qkv_parts = parts;
+  p.n_parts = n_parts;
+  p.parts_rows = parts_rows;
+  p.ld_qkv = ld_qkv;
+  p.rope_pos = pos;
+  p.rope_slot = slot;
+  p.rope_table = rope_table;
+  return launch_decode_tma(p, k_pool, v_pool, pool_blocks, n_items, q_heads, kv_heads, 128,
+                           block_size, max_kv_len, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
 }

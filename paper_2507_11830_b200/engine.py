@@ -337,6 +337,7 @@ class Engine:
         self.cuda_graphs = cuda_graphs
         self._fuse_splitk = os.environ.get("SP_FUSE_SPLITK", "1") != "0"
         self._fuse_rope = os.environ.get("SP_FUSE_ROPE", "1") != "0"
+        self._fuse_attn_rope = os.environ.get("SP_FUSE_ATTN_ROPE", "1") != "0"
         # fused decode layer (one persistent kernel per layer, P = 1 TP decode):
         # opt-in (SP_DECODE_FUSED=1) — measured slower than the kernel chain
         # ("fused decode layer")
@@ -652,8 +653,13 @@ class Engine:
         return self._ws
 
     # ------------------------------------------------------- shared pieces
-    def _attend(self, r: int, layer: int, q: torch.Tensor, out: torch.Tensor, meta: _Meta,
-                meter: FlopMeter, *, tails: bool = False) -> None:
+    def _attend(self, r: int, layer: int, q: Optional[torch.Tensor], out: torch.Tensor,
+                meta: _Meta, meter: FlopMeter, *, tails: bool = False, parts=None) -> None:
+        """Attention of one rank's heads (attend_cached loops, parallel_engine.py
+        :362-368 / :494-500).  ``parts`` = (QKV K-split partials, count) of a
+        decode pass: Q and the new token's RoPE + KV write are computed inside
+        the decode attention kernel (sp_attention_decode_qkv) instead of a
+        separate rope_kv_write_partials launch — bit-identical."""
         cfg = self.config
         P = self.world_size
         hq, hk, d = cfg.n_heads // P, cfg.kv_heads // P, cfg.head_dim
@@ -670,7 +676,14 @@ class Engine:
         hist = [w - m for m, w in zip(spans, meta.windows)]
         causal = sum(m * t0 + m * (m + 1) // 2 for m, t0 in zip(spans, hist))
         kv_bytes = sum(meta.windows) * hk * d * 2 * 2
-        if not tails and not decode_like and meta.n_combine is not None:
+        if parts is not None:
+            ops.attention_decode_qkv(parts[0], parts[1], meta.pos, meta.slots, self.weights.rope,
+                                     self.pool.layer_k(r, layer), self.pool.layer_v(r, layer),
+                                     meta.bt, cu, meta.kvlen, out, n_items=meta.n,
+                                     max_kv_len=meta.max_kv, q_heads=hq, kv_heads=hk,
+                                     block_size=self.pool.block_size, ws=ws,
+                                     work_flops=4 * d * hq * causal, work_bytes=kv_bytes)
+        elif not tails and not decode_like and meta.n_combine is not None:
             ops.attention_prefill_split(
                 q, self.pool.layer_k(r, layer), self.pool.layer_v(r, layer), meta.bt, cu, first,
                 meta.kvlen, out, work=meta.work_pairs, split=meta.work_split,
@@ -712,6 +725,13 @@ class Engine:
                           rows=meta.M if rows is None else rows, q_heads=hq,
                           kv_heads=cfg.kv_heads // P, head_dim=cfg.head_dim,
                           block_size=self.pool.block_size)
+
+    def _attn_rope_fusable(self, meta) -> bool:
+        """Decode pass whose attention runs on the TMA decode kernel (head_dim
+        128, pages of a multiple of 64 keys): RoPE + the KV write go into it
+        (SP_FUSE_ATTN_ROPE=0 keeps the separate kernel)."""
+        return (self._fuse_attn_rope and meta.decode_like and self.config.head_dim == 128
+                and self.pool.block_size % 64 == 0)
 
     def _fused_qkv_rope(self, M: int, hq: int, hk: int) -> bool:
         """QKV GEMM with RoPE + KV write in its epilogue: prefill-size passes
@@ -786,11 +806,15 @@ class Engine:
             for r in g.local_ranks:
                 q = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
                 n_qkv = self._partials(M, W, h)
+                fused_parts = None
                 if n_qkv > 1:  # decode: K-split partials reduced inside RoPE + KV write
                     qparts = torch.empty((n_qkv, M, W), dtype=torch.float32, device=dev)
                     ops.gemm(xn, lw.wqkv[r * W:(r + 1) * W], qparts, ops.EPI_PARTIAL_F32, M=M,
                              N=W, K=h, lda=h, ldb=h, ldd=W, meter=meters[r])
-                    self._kv_write(r, layer, None, q, meta, batch, parts=(qparts, n_qkv))
+                    if self._attn_rope_fusable(meta):  # ... or inside the decode attention
+                        fused_parts = (qparts, n_qkv)
+                    else:
+                        self._kv_write(r, layer, None, q, meta, batch, parts=(qparts, n_qkv))
                 elif self._fused_qkv_rope(M, hq, hk):
                     self._qkv_rope(r, layer, xn, lw.wqkv[r * W:(r + 1) * W], q, meta, hq, hk,
                                    meters[r])
@@ -800,7 +824,7 @@ class Engine:
                              K=h, lda=h, ldb=h, ldd=W, meter=meters[r])
                     self._kv_write(r, layer, qkv, q, meta, batch)
                 o = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
-                self._attend(r, layer, q, o, meta, meters[r])
+                self._attend(r, layer, q, o, meta, meters[r], parts=fused_parts)
                 wo = lw.wo[:, r * hqw:]
                 if P == 1:
                     split_pending = self._proj_residual(o, wo, x, M, h, hqw, cfg.n_heads * d,

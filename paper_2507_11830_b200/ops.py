@@ -457,6 +457,35 @@ def attention(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
     _lib.check(rc, "sp_attention")
 
 
+def attention_decode_qkv(parts: torch.Tensor, n_parts: int, pos: torch.Tensor,
+                         slot: torch.Tensor, rope: Optional[torch.Tensor], k_pool: torch.Tensor,
+                         v_pool: torch.Tensor, block_tables: torch.Tensor, cu_q: torch.Tensor,
+                         kv_len: torch.Tensor, out: torch.Tensor, *, n_items: int,
+                         max_kv_len: int, q_heads: int, kv_heads: int, block_size: int,
+                         ws: Optional[torch.Tensor], work_flops: int = 0,
+                         work_bytes: int = 0) -> None:
+    """Decode attention fed by the QKV K-split partials [n_parts, rows, W]
+    (sp_attention_decode_qkv): RoPE + the new token's KV write happen inside
+    the attention kernel; bit-identical to rope_kv_write_partials + attention."""
+    _need(parts, torch.float32, "attention_decode_qkv partials")
+    _need(out, torch.bfloat16, "attention out")
+    if n_items == 0:
+        return
+    width = (q_heads + 2 * kv_heads) * 128
+    rows = parts.numel() // max(1, n_parts * width)
+    if parts.numel() < n_parts * rows * width or rows < n_items:
+        raise ContractViolation("attention_decode_qkv: parts smaller than [n, rows, W]")
+    ws_bytes = 0 if ws is None else ws.numel() * ws.element_size()
+    with _Timed("attn_decode", work_flops, work_bytes):
+        rc = _lib.load().sp_attention_decode_qkv(
+            parts.data_ptr(), n_parts, width, rows, pos.data_ptr(), slot.data_ptr(), _ptr(rope),
+            k_pool.data_ptr(), v_pool.data_ptr(), k_pool.shape[0], block_tables.data_ptr(),
+            block_tables.stride(0), cu_q.data_ptr(), kv_len.data_ptr(), n_items, max_kv_len,
+            out.data_ptr(), out.stride(0), q_heads, kv_heads, block_size, _ptr(ws), ws_bytes,
+            _stream())
+    _lib.check(rc, "sp_attention_decode_qkv")
+
+
 SPLIT_SLOT_BYTES = 256 * 130 * 4  # one (work entry, kv head) partial: O [256][128] + (m, l)
 
 
