@@ -1267,8 +1267,11 @@ class Engine:
             self._stage_all(layer, batch)
             att = {}
             for r in g.local_ranks:
+                fused_parts = None
                 if isinstance(recv[r], _RopedQ):  # RoPE + KV write done in the QKV epilogue
                     q = recv[r].q
+                elif isinstance(recv[r], tuple) and self._attn_rope_fusable(meta):
+                    q, fused_parts = None, recv[r]  # ... or inside the decode attention (P = 1)
                 else:
                     q = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
                     if isinstance(recv[r], tuple):
@@ -1276,7 +1279,7 @@ class Engine:
                     else:
                         self._kv_write(r, layer, recv[r], q, meta, batch)
                 o = torch.empty((M, hqw), dtype=torch.bfloat16, device=dev)
-                self._attend(r, layer, q, o, meta, meters[r])
+                self._attend(r, layer, q, o, meta, meters[r], parts=fused_parts)
                 att[r] = o
             back = att
             if peer is not None:
