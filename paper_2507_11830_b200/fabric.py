@@ -183,6 +183,7 @@ class NcclGroup(DeviceGroup):
         # gloo cannot move CUDA tensors: stage through host memory (used to run
         # several ranks on ONE GPU in tests; B200 runs use NCCL directly)
         self._stage = dist.get_backend() == "gloo" and self.device.type == "cuda"
+        self._compact_idx: Dict[tuple, torch.Tensor] = {}  # all_gather_rows row indices
 
     def all_to_all(self, send, recv, in_splits, out_splits, row_bytes, group_size=None) -> None:
         me = self.rank
@@ -244,17 +245,42 @@ class NcclGroup(DeviceGroup):
         mx = max(counts) if counts else 0
         if p == 1:
             full = t[:counts[0]]
-        else:
+        elif self._stage:
             pad = torch.empty((mx, width), dtype=t.dtype, device=t.device)  # pad rows unread
             pad[:counts[me]].copy_(t[:counts[me]])
-            if self._stage:
-                chunks = [torch.empty((mx, width), dtype=t.dtype) for _ in range(p)]
-                self._dist.all_gather(chunks, pad.cpu())
-                buf = torch.cat(chunks, dim=0).to(t.device)
-            else:
-                buf = torch.empty((p * mx, width), dtype=t.dtype, device=t.device)
-                self._dist.all_gather_into_tensor(buf, pad)
+            chunks = [torch.empty((mx, width), dtype=t.dtype) for _ in range(p)]
+            self._dist.all_gather(chunks, pad.cpu())
+            buf = torch.cat(chunks, dim=0).to(t.device)
             full = torch.cat([buf[r * mx:r * mx + counts[r]] for r in range(p)], dim=0)
+        elif all(c == mx for c in counts) and t.is_contiguous():
+            # even shards: every rank's rows land in place (no pad, no compaction)
+            full = torch.empty((p * mx, width), dtype=t.dtype, device=t.device)
+            self._dist.all_gather_into_tensor(full, t[:mx])
+        else:
+            pad = t if (t.shape[0] >= mx and t.is_contiguous()) else None
+            if pad is None:  # this rank holds fewer rows: pad to the common block (rows unread)
+                pad = torch.empty((mx, width), dtype=t.dtype, device=t.device)
+                pad[:counts[me]].copy_(t[:counts[me]])
+            buf = torch.empty((p * mx, width), dtype=t.dtype, device=t.device)
+            self._dist.all_gather_into_tensor(buf, pad[:mx])
+            if t.device.type != "cuda":  # CPU (gloo) process groups: host compaction
+                full = torch.cat([buf[r * mx:r * mx + counts[r]] for r in range(p)], dim=0)
+                nbytes = sum(counts) * width * t.element_size()
+                self.charge("all_gather", [(p - 1) / p * nbytes] * p)
+                return full
+            # drop every block's pad rows with ONE row-gather kernel (index cached per counts)
+            key = tuple(counts)
+            idx = self._compact_idx.get(key)
+            if idx is None:
+                rows = [r * mx + i for r in range(p) for i in range(counts[r])]
+                idx = torch.tensor(rows, dtype=torch.int32, device=t.device)
+                self._compact_idx[key] = idx
+            full = torch.empty((idx.shape[0], width), dtype=t.dtype, device=t.device)
+            from . import ops
+            if t.dtype == torch.float32:
+                ops.gather_rows(buf, idx, full)
+            else:
+                ops.gather_rows_bf16(buf, idx, full)
         nbytes = sum(counts) * width * t.element_size()
         self.charge("all_gather", [(p - 1) / p * nbytes] * p)
         return full

@@ -106,3 +106,4 @@ def test_engine_decode_fused_attention_bitexact(P):
         assert torch.equal(runs[0][0], other[0])
         for a, b in zip(runs[0][1], other[1]):
             assert torch.equal(a, b)
+

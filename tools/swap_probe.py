@@ -12,15 +12,17 @@ from paper_2507_11830_b200 import ops  # noqa: E402
 
 M, N, K = (int(x) for x in sys.argv[1:4])
 epi = {"bf16": ops.EPI_STORE_BF16, "add": ops.EPI_ADD_F32, "swiglu": ops.EPI_SWIGLU, "gelu": ops.EPI_GELU,
-       "f32": ops.EPI_STORE_F32}[sys.argv[4] if len(sys.argv) > 4 else "bf16"]
+       "f32": ops.EPI_STORE_F32, "part": ops.EPI_PARTIAL_F32}[sys.argv[4] if len(sys.argv) > 4 else "bf16"]
 reps = int(sys.argv[5]) if len(sys.argv) > 5 else 20
 ops.set_gemm_workspace(torch.empty(64 << 20, dtype=torch.uint8, device="cuda"))
 a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
 nb = max(1, min(8, int((400 << 20) // (N * K * 2)) + 1))
 bs = [torch.randn(N, K, device="cuda").to(torch.bfloat16) for _ in range(nb)]
 ncol = N // 2 if epi == ops.EPI_SWIGLU else N
-d = torch.zeros(M, ncol, device="cuda",
-                dtype=torch.float32 if epi in (ops.EPI_ADD_F32, ops.EPI_STORE_F32) else torch.bfloat16)
+nslab = ops.gemm_partials(M, N, K) if epi == ops.EPI_PARTIAL_F32 else 1
+d = torch.zeros(nslab * M, ncol, device="cuda",
+                dtype=torch.float32 if epi in (ops.EPI_ADD_F32, ops.EPI_STORE_F32, ops.EPI_PARTIAL_F32)
+                else torch.bfloat16)
 for i in range(3):
     ops.gemm(a, bs[i % nb], d, epi, M=M, N=N, K=K, lda=K, ldb=K, ldd=ncol)
 torch.cuda.synchronize()
