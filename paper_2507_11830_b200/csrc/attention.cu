@@ -464,19 +464,20 @@ __device__ __forceinline__ void fence_proxy_async_global_() {
 // the QKV K-split partials: ascending sum, bf16 rounding, RoPE with
 // rope_rotate — the arithmetic of rope_kv_kernel (qkv_chunk) bit for bit.
 // Q goes to the swizzled sQ tile (rows >= G zero), K/V to the pool at the slot.
+template <bool kPlain = false>
 __device__ __forceinline__ void build_q_kv(const Params& p, __nv_bfloat16* sQ, int item, int kvh,
-                                           bool kv_writer, int tid) {
+                                           bool kv_writer, int tid, int nthreads = NCONS * 32) {
   const int G = p.group;
   const int row = p.cu_q[item];
   const int pos = p.rope_pos[row];
   const int slot = kv_writer ? p.rope_slot[row] : -1;
   // rows G..15 of the m16 Q tile are padding: zero them
-  for (int i = tid; i < (16 - G) * (HD / 8); i += NCONS * 32) {
+  for (int i = tid; i < (16 - G) * (HD / 8); i += nthreads) {
     const int r = G + i / (HD / 8), c = i % (HD / 8);
     *reinterpret_cast<uint4*>(sQ + r * HD + c * 8) = make_uint4(0, 0, 0, 0);
   }
   const int heads = G + (slot >= 0 ? 2 : 0);
-  for (int it = tid; it < heads * 16; it += NCONS * 32) {
+  for (int it = tid; it < heads * 16; it += nthreads) {
     const int hh = it >> 4, i0 = (it & 15) * 4;
     int col_head;
     bool rotate = p.rope_table != nullptr;
@@ -515,8 +516,13 @@ __device__ __forceinline__ void build_q_kv(const Params& p, __nv_bfloat16* sQ, i
     }
     if (hh < G) {
       __nv_bfloat16* rowp = sQ + hh * HD;
-      *reinterpret_cast<uint2*>(rowp + swz<HD>(hh, i0 >> 3) * 8 + (i0 & 7)) = make_uint2(ua[0], ua[1]);
-      *reinterpret_cast<uint2*>(rowp + swz<HD>(hh, (i0 + 64) >> 3) * 8 + (i0 & 7)) = make_uint2(ub[0], ub[1]);
+      if (kPlain) {
+        *reinterpret_cast<uint2*>(rowp + i0) = make_uint2(ua[0], ua[1]);
+        *reinterpret_cast<uint2*>(rowp + 64 + i0) = make_uint2(ub[0], ub[1]);
+      } else {
+        *reinterpret_cast<uint2*>(rowp + swz<HD>(hh, i0 >> 3) * 8 + (i0 & 7)) = make_uint2(ua[0], ua[1]);
+        *reinterpret_cast<uint2*>(rowp + swz<HD>(hh, (i0 + 64) >> 3) * 8 + (i0 & 7)) = make_uint2(ub[0], ub[1]);
+      }
     } else {
       __nv_bfloat16* pool = const_cast<__nv_bfloat16*>(hh == G ? p.k_pool : p.v_pool);
       const int64_t blk = slot / p.block_size, off = slot % p.block_size;
@@ -711,6 +717,297 @@ __global__ void __launch_bounds__(NUM_THREADS, 2) decode_tma_kernel(
     }
   }
 }
+
+// ------------------------------------------------ tcgen05 / TMEM decode
+// Same CTA decomposition, TMA producer, KV splits and fused-QKV path as
+// decode_tma_kernel, with the tensor-core work on tcgen05: Q (the CTA's G <= 16
+// q heads, padded to the M = 128 MMA rows — TMEM rows are independent, the
+// padding rows are never read) lives in TMEM as the A operand; per 64-key page
+// slice S = Q . K^T (M128 N64, K from the ring) lands in TMEM, one softmax warp
+// (lane = q head) turns it into P in place (bf16 over the first 32 columns of
+// S), and O += P . V (P from TMEM, V MN-major from the ring) accumulates in
+// TMEM.  TMEM: Q 0-63 | S 64-127 | O 128-255 (256 columns: two CTAs per SM).
+// Online softmax with the lazy rescale of the prefill kernel; outputs /
+// split partials in the format of decode_tma_kernel (same combine kernel).
+constexpr int TC_THREADS = 96;  // warp 0 softmax + epilogue, warp 1 TMA producer, warp 2 MMA
+constexpr int TC_SMEM = STAGES * STAGE_BYTES + 16 * HD * 2 + 1024 + 256;
+
+__global__ void __launch_bounds__(TC_THREADS, 2) decode_tc_kernel(
+    const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Params p) {
+  pdl_trigger();
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem + STAGES * STAGE_BYTES);  // [16][HD] plain
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + 16 * HD * 2);
+  uint64_t* empty = full + STAGES;
+  uint64_t* kv_ready = empty + STAGES;
+  uint64_t* q_ready = kv_ready + 1;  // Q stored in TMEM
+  uint64_t* s_full = q_ready + 1;
+  uint64_t* p_ready = s_full + 1;
+  uint64_t* o_full = p_ready + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int item = blockIdx.x, kvh = blockIdx.y, split = blockIdx.z;
+  const int G = p.group;
+  const int q_row = p.cu_q[item];
+  const int kv_len = p.kv_len[item];
+  const int32_t* bt = p.block_tables + (int64_t)item * p.bt_stride;
+  const int n_tiles = (kv_len + PAGE - 1) / PAGE;
+  const int per_split = (n_tiles + p.n_splits - 1) / p.n_splits;
+  const int t_begin = split * per_split;
+  const int t_end = min(n_tiles, t_begin + per_split);
+  const int n_sl = max(t_end - t_begin, 0);
+
+  if (warp == 1 && lane == 0) {
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(kv_ready, 1);
+    mbar_init(q_ready, 1);
+    mbar_init(s_full, 1);
+    mbar_init(p_ready, 1);
+    mbar_init(o_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t q_tmem = tmem, s_tmem = tmem + 64, o_tmem = tmem + 128;
+  const bool kv_writer = p.qkv_parts != nullptr && t_begin <= n_tiles - 1 && n_tiles - 1 < t_end;
+
+  if (warp == 1) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      const int old_tiles = (kv_len - 1) / PAGE;
+      bool waited = false;
+      for (int t = t_begin, i = 0; t < t_end; ++t, ++i) {
+        if (!waited && (i >= STAGES || t >= old_tiles)) {
+          pdl_wait();
+          waited = true;
+        }
+        if (kv_writer && t == old_tiles) mbar_wait(kv_ready, 0);
+        const int s = i % STAGES;
+        mbar_wait(empty + s, ((i / STAGES) & 1) ^ 1);
+        const int key0 = t * PAGE;
+        const int page = bt[key0 / p.block_size];
+        const int row = (page * p.kv_heads + kvh) * p.block_size + key0 % p.block_size;
+        uint8_t* st = smem + s * STAGE_BYTES;
+        mbar_arrive_expect_tx(full + s, STAGE_BYTES);
+        if (p.kv_stream) {
+          const uint64_t pol = l2_evict_first_policy();
+          tma_load_2d_hint(st, &tmK, full + s, 0, row, pol);
+          tma_load_2d_hint(st + TILE_BYTES / 2, &tmK, full + s, 64, row, pol);
+          tma_load_2d_hint(st + TILE_BYTES, &tmV, full + s, 0, row, pol);
+          tma_load_2d_hint(st + TILE_BYTES + TILE_BYTES / 2, &tmV, full + s, 64, row, pol);
+        } else {
+          tma_load_2d(st, &tmK, full + s, 0, row);
+          tma_load_2d(st + TILE_BYTES / 2, &tmK, full + s, 64, row);
+          tma_load_2d(st + TILE_BYTES, &tmV, full + s, 0, row);
+          tma_load_2d(st + TILE_BYTES + TILE_BYTES / 2, &tmV, full + s, 64, row);
+        }
+      }
+      if (!waited) pdl_wait();
+    }
+    __syncwarp();
+  } else {
+    // -------------------------------------- Q into TMEM (warps 0 and 2 build it)
+    pdl_wait();  // Q (or the QKV partials) is written by the predecessor
+    const int ctid = warp == 0 ? lane : 32 + lane;
+    if (p.qkv_parts != nullptr) {
+      build_q_kv<true>(p, sQ, item, kvh, kv_writer, ctid, 64);
+      if (kv_writer) fence_proxy_async_global_();  // pool writes -> this CTA's TMA loads
+    } else {
+      for (int i = ctid; i < G * (HD / 8); i += 64) {
+        const int r = i / (HD / 8), c = i % (HD / 8);
+        *reinterpret_cast<uint4*>(sQ + r * HD + c * 8) =
+            *reinterpret_cast<const uint4*>(p.q + (int64_t)q_row * p.ldq + (int64_t)(kvh * G + r) * HD + c * 8);
+      }
+    }
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+    if (warp == 2 && kv_writer && lane == 0) mbar_arrive(kv_ready);
+    if (warp == 0) {
+      // row = lane: its 128 d as 64 bf16x2 columns (lanes >= G: zeros)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t r[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          r[e] = lane < G ? *reinterpret_cast<const uint32_t*>(sQ + lane * HD + c * 64 + 2 * e) : 0u;
+        tmem_st32(q_tmem + c * 32, r);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_ready);
+    }
+      if (warp == 2) {
+    // ---------------------------------------------------------- MMA issuer
+    if (lane == 0 && n_sl > 0) {
+      constexpr uint32_t idesc_qk = idesc_bf16_f32(128, PAGE);
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(128, HD) | (1u << 16);  // V MN-major
+      mbar_wait(q_ready, 0);
+      tc_fence_after();
+      for (int i = 0; i <= n_sl; ++i) {
+        if (i > 0) {  // P(i-1) . V(i-1), then release the slice
+          mbar_wait(p_ready, (i - 1) & 1);
+          tc_fence_after();
+          const uint32_t sv = smem_u32(smem + ((i - 1) % STAGES) * STAGE_BYTES + TILE_BYTES);
+#pragma unroll
+          for (int k = 0; k < PAGE / 16; ++k)
+            umma_ts_bf16(o_tmem, s_tmem + k * 8, sdesc_sw128_mn(sv + k * 2048, TILE_BYTES / 2),
+                         idesc_pv, (i > 1 || k > 0) ? 1u : 0u);
+          umma_commit(empty + (i - 1) % STAGES);
+          if (i == n_sl) umma_commit(o_full);
+        }
+        if (i < n_sl) {  // S(i) = Q . K(i)^T (after P(i-1) is consumed: same columns)
+          const int s = i % STAGES;
+          mbar_wait(full + s, (i / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t sk = smem_u32(smem + s * STAGE_BYTES);
+#pragma unroll
+          for (int k = 0; k < HD / 16; ++k)
+            umma_ts_bf16(s_tmem, q_tmem + k * 8,
+                         sdesc_sw128(sk + (k >> 2) * (TILE_BYTES / 2) + (k & 3) * 32), idesc_qk,
+                         k > 0 ? 1u : 0u);
+          umma_commit(s_full);
+        }
+      }
+    }
+    __syncwarp();
+      } else {
+    // ------------------------------------------------------ softmax / epilogue
+    float m_run = -INFINITY, l_run = 0.f;
+    const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2);
+    for (int i = 0; i < n_sl; ++i) {
+      mbar_wait(s_full, i & 1);
+      tc_fence_after();
+      float sv[PAGE];
+      {
+        uint32_t r[2][32];
+        tmem_ld32(s_tmem, r[0]);
+        tmem_ld32(s_tmem + 32, r[1]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int e = 0; e < 32; ++e) sv[c * 32 + e] = __uint_as_float(r[c][e]);
+      }
+      const int kbase = (t_begin + i) * PAGE;
+      if (kbase + PAGE > kv_len) {
+#pragma unroll
+        for (int e = 0; e < PAGE; ++e)
+          if (kbase + e >= kv_len) sv[e] = -INFINITY;
+      }
+      float mxs[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) mxs[q] = fmaxf(sv[2 * q], sv[2 * q + 1]);
+#pragma unroll
+      for (int e = 16; e < PAGE; e += 16)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mxs[q] = fmaxf(mxs[q], fmaxf(sv[e + 2 * q], sv[e + 2 * q + 1]));
+#pragma unroll
+      for (int w = 4; w; w >>= 1)
+#pragma unroll
+        for (int q = 0; q < w; ++q) mxs[q] = fmaxf(mxs[q], mxs[q + w]);
+      const float m_new = fmaxf(m_run, mxs[0] * p.scale_log2);
+      const bool need = m_new > m_run + 8.0f;
+      float corr = 1.f;
+      if (need) {
+        corr = fast_exp2(m_run - m_new);
+        m_run = m_new;
+      }
+      l_run *= corr;
+      if (i > 0 && __any_sync(0xffffffffu, need)) {  // P.V(i-1) is complete (covered by s_full)
+#pragma unroll 1
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(o_tmem + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * corr);
+          tmem_st32(o_tmem + c * 32, r);
+        }
+        tmem_st_wait();
+      }
+      const uint64_t nm2 = f2_pack(-m_run, -m_run);
+      uint64_t sums[4] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
+      uint32_t pk[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        float a, b;
+        const uint64_t x2 = f2_fma(f2_pack(sv[2 * e], sv[2 * e + 1]), sc2, nm2);
+        f2_unpack(x2, a, b);
+        a = fast_exp2(a);
+        b = fast_exp2(b);
+        sums[e & 3] = f2_add(sums[e & 3], f2_pack(a, b));
+        pk[e] = pack_bf16x2(a, b);
+      }
+      tmem_st32(s_tmem, pk);
+      const uint64_t sum2 = f2_add(f2_add(sums[0], sums[1]), f2_add(sums[2], sums[3]));
+      float sa, sb;
+      f2_unpack(sum2, sa, sb);
+      l_run += sa + sb;
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_ready);
+    }
+    // epilogue: row = lane (q head kvh * G + lane)
+    float o[HD];
+    if (n_sl > 0) {
+      mbar_wait(o_full, 0);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(o_tmem + c * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) o[c * 32 + e] = __uint_as_float(r[e]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < HD; ++e) o[e] = 0.f;
+    }
+    if (lane < G) {
+      const int qh = kvh * G + lane;
+      const bool ok = l_run > 0.f;
+      const float inv = ok ? 1.f / l_run : 0.f;
+      if (p.n_splits == 1) {
+        uint4* d4 = reinterpret_cast<uint4*>(p.out + (int64_t)q_row * p.ldo + (int64_t)qh * HD);
+#pragma unroll
+        for (int q = 0; q < HD / 8; ++q) {
+          uint4 u;
+          u.x = pack_bf16x2(o[8 * q + 0] * inv, o[8 * q + 1] * inv);
+          u.y = pack_bf16x2(o[8 * q + 2] * inv, o[8 * q + 3] * inv);
+          u.z = pack_bf16x2(o[8 * q + 4] * inv, o[8 * q + 5] * inv);
+          u.w = pack_bf16x2(o[8 * q + 6] * inv, o[8 * q + 7] * inv);
+          d4[q] = u;
+        }
+      } else {
+        const int64_t slot = ((int64_t)item * p.q_heads + qh) * p.n_splits + split;
+        float4* w4 = reinterpret_cast<float4*>(p.ws_o + slot * HD);
+#pragma unroll
+        for (int q = 0; q < HD / 4; ++q)
+          w4[q] = make_float4(o[4 * q] * inv, o[4 * q + 1] * inv, o[4 * q + 2] * inv, o[4 * q + 3] * inv);
+        p.ws_lse[slot] = ok ? m_run + log2f(l_run) : -INFINITY;
+      }
+    }
+      }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
 }  // namespace dec
 
 static int decode_tma_splits(int n_items, int kv_heads, int max_kv_len) {
@@ -829,11 +1126,23 @@ static sp_status launch_decode_tma(attn::Params& p, const void* k_pool, const vo
   if (!attr) {
     cudaFuncSetAttribute(attn::dec::decode_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          attn::dec::SMEM_BYTES);
+    cudaFuncSetAttribute(attn::dec::decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         attn::dec::TC_SMEM);
     attr = true;
   }
-  launch_k(attn::dec::decode_tma_kernel, dim3(n_items, kv_heads, p.n_splits), attn::dec::NUM_THREADS,
-           attn::dec::SMEM_BYTES, st, tk, tv, p);
-  if (int rc = check_launch("attn_decode_tma_kernel")) return rc;
+  // SP_DECODE_TC=1: the tcgen05/TMEM consumer (opt-in: equal in isolation but
+  // slower in-graph, where its 256 TMEM columns per CTA contend with the
+  // PDL-overlapped projections — DESIGN.md §10); read per call (tests A/B it)
+  const char* tce = getenv("SP_DECODE_TC");
+  if (tce && tce[0] == '1' && p.group <= 16) {
+    launch_k(attn::dec::decode_tc_kernel, dim3(n_items, kv_heads, p.n_splits), attn::dec::TC_THREADS,
+             attn::dec::TC_SMEM, st, tk, tv, p);
+    if (int rc = check_launch("attn_decode_tc_kernel")) return rc;
+  } else {
+    launch_k(attn::dec::decode_tma_kernel, dim3(n_items, kv_heads, p.n_splits), attn::dec::NUM_THREADS,
+             attn::dec::SMEM_BYTES, st, tk, tv, p);
+    if (int rc = check_launch("attn_decode_tma_kernel")) return rc;
+  }
   if (p.n_splits > 1) {
     launch_k(attn::combine_kernel, dim3(n_items, q_heads), head_dim, 0, st, p, head_dim);
     return check_launch("attn_combine_kernel");

@@ -34,7 +34,9 @@ def _dev():
     (64, 900, 32, 8, 64, 7),      # one split per (item, kv head)
     (3, 1500, 64, 8, 64, 5),      # 70B-style group of 8
 ])
-def test_decode_qkv_kernel_bitexact(B, ctx, hq, hk, bs, n_parts):
+@pytest.mark.parametrize("tc", ["0", "1"])
+def test_decode_qkv_kernel_bitexact(B, ctx, hq, hk, bs, n_parts, tc, monkeypatch):
+    monkeypatch.setenv("SP_DECODE_TC", tc)  # mma.sync or tcgen05/TMEM decode consumers
     torch.manual_seed(B * 7 + ctx)
     d = 128
     W = (hq + 2 * hk) * d

@@ -263,9 +263,13 @@ def test_attention_prefill_paged_causal(d, hq, hk, bs):
 @pytest.mark.parametrize("d,hq,hk,ctx", [(128, 32, 8, 2048), (128, 8, 2, 100), (64, 4, 4, 5000),
                                          (32, 8, 2, 1), (128, 8, 2, 5000), (128, 32, 2, 700),
                                          (128, 64, 8, 300)])
-def test_attention_decode_split_kv(d, hq, hk, ctx):
+@pytest.mark.parametrize("tc", ["0", "1"])
+def test_attention_decode_split_kv(d, hq, hk, ctx, tc, monkeypatch):
     """Split-KV decode (TMA kernel with the first ring of old pages streamed
-    before the PDL wait; splits merged by the combine kernel) vs the reference."""
+    before the PDL wait; splits merged by the combine kernel) vs the reference,
+    with the mma.sync consumers (tc=0) and the tcgen05/TMEM ones (tc=1: Q as
+    the TMEM A operand, S and O in TMEM; d=128 only)."""
+    monkeypatch.setenv("SP_DECODE_TC", tc)
     n = 5
     bs = 64
     ctxs = [ctx + 7 * i for i in range(n)]
