@@ -492,11 +492,20 @@ __device__ __forceinline__ void build_q_kv(const Params& p, __nv_bfloat16* sQ, i
     const float* src = p.qkv_parts + (int64_t)row * p.ld_qkv + (int64_t)col_head * HD + i0;
     const int64_t pstride = (int64_t)p.parts_rows * p.ld_qkv;
     float a[4] = {0.f, 0.f, 0.f, 0.f}, b[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int sidx = 0; sidx < p.n_parts; ++sidx) {
-      const float4 x = *reinterpret_cast<const float4*>(src + sidx * pstride);
-      const float4 y = *reinterpret_cast<const float4*>(src + sidx * pstride + 64);
-      a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
-      b[0] += y.x; b[1] += y.y; b[2] += y.z; b[3] += y.w;
+    for (int s0 = 0; s0 < p.n_parts; s0 += 8) {  // 8 slabs' loads in flight, summed in order
+      float4 xs[8], ys[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const bool ok = s0 + k < p.n_parts;
+        xs[k] = ok ? *reinterpret_cast<const float4*>(src + (s0 + k) * pstride) : make_float4(0.f, 0.f, 0.f, 0.f);
+        ys[k] = ok ? *reinterpret_cast<const float4*>(src + (s0 + k) * pstride + 64) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (s0 + k >= p.n_parts) break;
+        a[0] += xs[k].x; a[1] += xs[k].y; a[2] += xs[k].z; a[3] += xs[k].w;
+        b[0] += ys[k].x; b[1] += ys[k].y; b[2] += ys[k].z; b[3] += ys[k].w;
+      }
     }
     uint32_t ua[2] = {pack_bf16x2(a[0], a[1]), pack_bf16x2(a[2], a[3])};
     uint32_t ub[2] = {pack_bf16x2(b[0], b[1]), pack_bf16x2(b[2], b[3])};
@@ -729,7 +738,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2) decode_tma_kernel(
 // TMEM.  TMEM: Q 0-63 | S 64-127 | O 128-255 (256 columns: two CTAs per SM).
 // Online softmax with the lazy rescale of the prefill kernel; outputs /
 // split partials in the format of decode_tma_kernel (same combine kernel).
-constexpr int TC_THREADS = 96;  // warp 0 softmax + epilogue, warp 1 TMA producer, warp 2 MMA
+constexpr int TC_THREADS = 128;  // warp 0 softmax + epilogue, 1 TMA producer, 2 MMA, 3 (+0, 2) Q build
 constexpr int TC_SMEM = STAGES * STAGE_BYTES + 16 * HD * 2 + 1024 + 256;
 
 __global__ void __launch_bounds__(TC_THREADS, 2) decode_tc_kernel(
@@ -816,20 +825,20 @@ __global__ void __launch_bounds__(TC_THREADS, 2) decode_tc_kernel(
     }
     __syncwarp();
   } else {
-    // -------------------------------------- Q into TMEM (warps 0 and 2 build it)
+    // -------------------------------- Q into TMEM (warps 0, 2 and 3 build it)
     pdl_wait();  // Q (or the QKV partials) is written by the predecessor
-    const int ctid = warp == 0 ? lane : 32 + lane;
+    const int ctid = warp == 0 ? lane : (warp == 2 ? 32 : 64) + lane;
     if (p.qkv_parts != nullptr) {
-      build_q_kv<true>(p, sQ, item, kvh, kv_writer, ctid, 64);
+      build_q_kv<true>(p, sQ, item, kvh, kv_writer, ctid, 96);
       if (kv_writer) fence_proxy_async_global_();  // pool writes -> this CTA's TMA loads
     } else {
-      for (int i = ctid; i < G * (HD / 8); i += 64) {
+      for (int i = ctid; i < G * (HD / 8); i += 96) {
         const int r = i / (HD / 8), c = i % (HD / 8);
         *reinterpret_cast<uint4*>(sQ + r * HD + c * 8) =
             *reinterpret_cast<const uint4*>(p.q + (int64_t)q_row * p.ldq + (int64_t)(kvh * G + r) * HD + c * 8);
       }
     }
-    asm volatile("bar.sync 1, 64;" ::: "memory");
+    asm volatile("bar.sync 1, 96;" ::: "memory");
     if (warp == 2 && kv_writer && lane == 0) mbar_arrive(kv_ready);
     if (warp == 0) {
       // row = lane: its 128 d as 64 bf16x2 columns (lanes >= G: zeros)
@@ -880,7 +889,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) decode_tc_kernel(
       }
     }
     __syncwarp();
-      } else {
+      } else if (warp == 0) {
     // ------------------------------------------------------ softmax / epilogue
     float m_run = -INFINITY, l_run = 0.f;
     const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2);
