@@ -148,6 +148,43 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ x, int64_t ldx, const flo
   }
 }
 
+// RMSNorm without a residual add (the prefill norms: the projection epilogue
+// already added the residual), register-lean so that 6+ CTAs per SM keep
+// enough row bytes in flight (the general kernel's 76 registers allowed 3 and
+// reached half the HBM bandwidth): the gains are loaded only for the store
+// (L2-resident), not held across the reduction.  Same block size and chunk
+// order -> bit-identical to add_rmsnorm_kernel.
+template <int VEC, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    rmsnorm_lean_kernel(const float* __restrict__ x, int64_t ldx, const float* __restrict__ gain,
+                        float eps, __nv_bfloat16* __restrict__ out, int64_t ldo, int hidden) {
+  pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
+  pdl_wait();  // x is written by the predecessor
+  const int64_t r = blockIdx.x;
+  const float* xr = x + r * ldx;
+  float4 v[VEC];
+  float ssq[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = (i * blockDim.x + threadIdx.x) * 4;
+    v[i] = c < hidden ? __ldcs(reinterpret_cast<const float4*>(xr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) ssq[i] = norm_sq4(v[i]);
+  __shared__ float red[256];
+  const float ss = rms_chunk_sum<VEC>(ssq, hidden, red);
+  const float den = norm_den(ss, hidden, eps);
+  __nv_bfloat16* orow = out + r * ldo;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = (i * blockDim.x + threadIdx.x) * 4;
+    if (c < hidden) {
+      const float4 g = __ldg(reinterpret_cast<const float4*>(gain + c));
+      *reinterpret_cast<uint2*>(orow + c) = norm_pack4(g, v[i].x, v[i].y, v[i].z, v[i].w, den);
+    }
+  }
+}
+
 // ------------------------------------------------- RoPE + paged KV write
 // 8 threads per (token, head): thread j owns rotation pairs [8j, 8j+8) of a
 // 128-dim head (16-byte loads of both halves, one float4x2 of cos/sin each);
@@ -398,6 +435,13 @@ extern "C" sp_status sp_add_rmsnorm(float* x, int64_t ldx, const float* add, int
   if (const char* e = getenv("SP_NORM_THREADS")) threads = atoi(e);
   const int per = (hidden + threads * 4 - 1) / (threads * 4);
   auto out = static_cast<__nv_bfloat16*>(out_bf16);
+  // many rows, no residual add, no gather: the register-lean kernel (SP_NORM_LEAN=0: general)
+  const char* lean = getenv("SP_NORM_LEAN");
+  if (!add && !row_idx && out && rows > 2 * 148 && threads == 256 && per == 4 &&
+      !(lean && lean[0] == '0')) {
+    launch_k(rmsnorm_lean_kernel<4, 6>, rows, threads, 0, S(stream), x, ldx, gain, eps, out, ldo, hidden);
+    return check_launch("rmsnorm_lean_kernel");
+  }
   switch (per) {
     case 1: launch_k(add_rmsnorm_kernel<1>, rows, threads, 0, S(stream), x, ldx, add, n_add, add_stride, gain, eps, row_idx, out, ldo, hidden); break;
     case 2: launch_k(add_rmsnorm_kernel<2>, rows, threads, 0, S(stream), x, ldx, add, n_add, add_stride, gain, eps, row_idx, out, ldo, hidden); break;
