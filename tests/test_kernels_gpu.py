@@ -598,6 +598,26 @@ def test_rmsnorm_block_size_invariant(h):
     assert torch.equal(small, big[:few])
 
 
+@pytest.mark.parametrize("rows", [297, 1000, 8192])
+def test_rmsnorm_lean_kernel_bitexact(rows, monkeypatch):
+    """The prefill norm (no residual add, hidden 4096, many rows) runs on the
+    register-lean kernel; it must equal the general add+RMSNorm kernel bit for
+    bit, and the few-row (decode) norm of the same rows as well."""
+    h = 4096
+    x = torch.randn(rows, h, device="cuda") * 2
+    gain = torch.rand(h, device="cuda") + 0.5
+    outs = []
+    for lean in ("0", "1"):
+        monkeypatch.setenv("SP_NORM_LEAN", lean)
+        o = torch.empty(rows, h, device="cuda", dtype=torch.bfloat16)
+        ops.add_rmsnorm(x, gain, 1e-5, o)
+        outs.append(o)
+    assert torch.equal(outs[0], outs[1])
+    few = torch.empty(5, h, device="cuda", dtype=torch.bfloat16)
+    ops.add_rmsnorm(x[:5].clone(), gain, 1e-5, few)  # wide-block decode path
+    assert torch.equal(few, outs[1][:5])
+
+
 @pytest.mark.parametrize("chunk", [1, 2, 3])
 def test_attention_prefill_split_kv(chunk):
     """Split-KV tcgen05 prefill: each work tile's key tiles cut into ranges of
