@@ -19,8 +19,8 @@ B = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 CTX = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
 cfg = llama31_8b(max_seq=CTX + 64)
 w = ModelWeights.random(cfg, seed=0, world_size=1)
-orig = {k: getattr(ops, k) for k in ("gemm", "attention", "add_rmsnorm", "rope_kv_write",
-                                     "rope_kv_write_partials")}
+orig = {k: getattr(ops, k) for k in ("gemm", "attention", "attention_decode_qkv", "add_rmsnorm",
+                                     "rope_kv_write", "rope_kv_write_partials")}
 
 
 def run(label, skip):
@@ -32,7 +32,8 @@ def run(label, skip):
                 return
             return orig["gemm"](a, b, d, epi, M=M, N=N, K=K, **kw)
         ops.gemm = gemm
-        for k in ("attention", "add_rmsnorm", "rope_kv_write", "rope_kv_write_partials"):
+        for k in ("attention", "attention_decode_qkv", "add_rmsnorm", "rope_kv_write",
+                  "rope_kv_write_partials"):
             if k in skip:
                 setattr(ops, k, lambda *a, **kw: None)
     eng = Engine(w, LoopbackGroup(1), ShiftPolicy.fixed_tp(), num_blocks=B * -(-(CTX + 64) // 64) + 8)
@@ -69,7 +70,10 @@ h, f, W = cfg.hidden, cfg.ffn_dim, w.qkv_width
 base = run("baseline", None)
 if len(sys.argv) > 3 and sys.argv[3] == "base":
     sys.exit(0)
-for label, skip in [("- attention", {"attention": 1}),
+# decode passes run RoPE + the KV write inside the attention kernel
+# (attention_decode_qkv) unless SP_FUSE_ATTN_ROPE=0: the attention row then
+# covers both and the rope row is empty
+for label, skip in [("- attention (+rope/kv)", {"attention": 1, "attention_decode_qkv": 1}),
                     ("- qkv gemm", {"gemm": [(W, h)]}),
                     ("- o gemm", {"gemm": [(h, cfg.n_heads * cfg.head_dim)]}),
                     ("- gate_up gemm", {"gemm": [(2 * f, h)]}),
