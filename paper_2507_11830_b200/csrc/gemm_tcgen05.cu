@@ -98,8 +98,18 @@ constexpr int kMaxPeerMaps = 8;
 struct PeerMaps {
   CUtensorMap m[kMaxPeerMaps];
   int n;
+  // EPI_ADD_F32 through TMA (pair kernel): m[0] is an f32 map of D, box 32 x
+  // 32 with 128-B swizzle; each epilogue warp TMA-loads its rows' old residual
+  // box, adds the accumulator in shared memory and TMA-stores it back — whole
+  // 128-B lines per instruction instead of 32 row-strided lines per warp access
+  int add_tma;
 };
 static thread_local const unsigned long long* t_peer_ptrs_host = nullptr;
+
+static bool add_tma_enabled() {  // SP_ADD_TMA=0: direct residual-add stores (A/B runs)
+  const char* e = getenv("SP_ADD_TMA");
+  return !(e && e[0] == '0');
+}
 
 static bool peer_tma_enabled() {  // SP_PEER_TMA=0: direct epilogue stores (A/B runs)
   const char* e = getenv("SP_PEER_TMA");
@@ -765,10 +775,14 @@ constexpr int A_BYTES = 128 * BK * 2;
 constexpr int B_BYTES = 128 * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
-// peer-TMA variant: + per-epilogue-warp 4 KiB staging boxes [32 rows][64 cols]
+// TMA-epilogue variants: per-epilogue-warp staging boxes — peer exchange: one
+// 4 KiB box [32 rows][64 bf16] at quarter * 4096; residual add: two 4 KiB
+// boxes [32 rows][32 f32] at quarter * 8192 (double-buffered loads)
 constexpr int OUT_OFF = STAGES * STAGE_BYTES + 1024;  // past the barriers, 1024-aligned
-constexpr int OUT_BYTES = 4 * 4096;
-constexpr int SMEM_BYTES_TMA = OUT_OFF + OUT_BYTES + 1024;
+constexpr int OUT_BYTES = 8 * 4096;
+constexpr int OUT_BAR_OFF = OUT_OFF + OUT_BYTES;      // 8 box-load barriers (residual add)
+constexpr int SMEM_BYTES_TMA = OUT_BAR_OFF + 64 + 1024;
+static_assert(SMEM_BYTES_TMA <= 232448, "pair TMA-epilogue smem over the 227 KiB limit");
 
 __device__ __forceinline__ uint32_t cta_rank() {
   uint32_t r;
@@ -848,6 +862,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     for (int a = 0; a < ACC_STAGES; ++a) {
       mbar_init(tfull + a, 1);
       mbar_init(tempty + a, 8);  // 4 epilogue warps x 2 CTAs (leader's barrier is used)
+    }
+    if (pm.add_tma) {
+      tma_prefetch_desc(&pm.m[0]);
+      for (int i = 0; i < 8; ++i) mbar_init(reinterpret_cast<uint64_t*>(smem + pair::OUT_BAR_OFF) + i, 1);
     }
     fence_barrier_init();
   }
@@ -975,6 +993,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           for (int j = 0; j < 32; ++j) v[j] = silu(__uint_as_float(g[j])) * __uint_as_float(u[j]);
           store_chunk(p, m, nb * 128 + c, v, SP_EPI_STORE_BF16, p.N / 2);
         }
+      } else if (pm.add_tma) {
+        // residual add through TMA: per 32-column chunk the warp's old x box
+        // [32 rows][32 f32] (128-B swizzled) is TMA-loaded one chunk ahead,
+        // each lane adds its row's accumulator (old + acc, the order of
+        // store_chunk) in shared memory, and one TMA store writes it back
+        uint8_t* stage = smem + pair::OUT_OFF + quarter * 8192;
+        uint64_t* lbar = reinterpret_cast<uint64_t*>(smem + pair::OUT_BAR_OFF) + quarter * 2;
+        const int mrow0 = mb * 256 + rank * 128 + quarter * 32;
+        const int ncol0 = nb * 256;
+        if (lane == 0) {
+          bulk_wait_read1();  // buffer 0's last store (two chunks back) has left smem
+          mbar_arrive_expect_tx(lbar, 4096);
+          tma_load_2d(stage, &pm.m[0], lbar, ncol0, mrow0);
+        }
+#pragma unroll 1
+        for (int k = 0; k < 8; ++k) {
+          uint8_t* box = stage + (k & 1) * 4096;
+          if (k + 1 < 8 && lane == 0) {
+            bulk_wait_read0();  // the store of chunk k-1 (the other buffer) has left smem
+            mbar_arrive_expect_tx(lbar + ((k + 1) & 1), 4096);
+            tma_load_2d(stage + ((k + 1) & 1) * 4096, &pm.m[0], lbar + ((k + 1) & 1),
+                        ncol0 + (k + 1) * 32, mrow0);
+          }
+          uint32_t r[32];
+          tmem_ld32(tb + k * 32, r);
+          tmem_ld_wait();
+          mbar_wait(lbar + (k & 1), (uint32_t)(k >> 1) & 1);  // 4 uses per buffer per tile
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4* q = reinterpret_cast<float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4));
+            float4 o = *q;
+            o.x += __uint_as_float(r[4 * j + 0]);
+            o.y += __uint_as_float(r[4 * j + 1]);
+            o.z += __uint_as_float(r[4 * j + 2]);
+            o.w += __uint_as_float(r[4 * j + 3]);
+            *q = o;
+          }
+          fence_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&pm.m[0], box, ncol0 + k * 32, mrow0);
+            bulk_commit();
+          }
+        }
       } else if (pm.n > 0) {
         // fused seq->head exchange (bf16): each warp stages its 32 rows x 64
         // columns in a 128-B-swizzled box and one TMA store writes it into the
@@ -1038,7 +1100,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
     }
   }
-  if (pm.n > 0 && warp >= 2 && (threadIdx.x & 31) == 0) bulk_wait0();  // stores landed
+  if ((pm.n > 0 || pm.add_tma) && warp >= 2 && (threadIdx.x & 31) == 0)
+    bulk_wait0();  // stores landed
   tc_fence_before();
   pair::cluster_sync();
   if (warp == 1) {
@@ -1148,10 +1211,11 @@ static int encoder() {
   return kOk;
 }
 
-// bf16 tiled map with 128-byte swizzle; dims/strides innermost first
+// tiled map with 128-byte swizzle (bf16 unless f32); dims/strides innermost first
 int get_map(CUtensorMap* out, const void* ptr, int rank, const uint64_t* dims,
-                   const uint64_t* strides, const uint32_t* box) {
+                   const uint64_t* strides, const uint32_t* box, bool f32 = false) {
   std::array<uint64_t, 12> key{};
+  key[11] = f32 ? 1 : 0;
   key[0] = reinterpret_cast<uint64_t>(ptr);
   key[1] = rank;
   for (int i = 0; i < rank; ++i) key[2 + i] = dims[i];
@@ -1165,7 +1229,7 @@ int get_map(CUtensorMap* out, const void* ptr, int rank, const uint64_t* dims,
   }
   if (int rc = encoder()) return rc;
   uint32_t estr[3] = {1, 1, 1};
-  CUresult r = g_encode(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr),
+  CUresult r = g_encode(out, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr),
                         dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1424,6 +1488,15 @@ static int launch_pair(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   choose_raster(p, 256, 256, K, M, N);
   PeerMaps pm;
   pm.n = 0;
+  pm.add_tma = 0;
+  if (epilogue == SP_EPI_ADD_F32 && peer_width == 0 && add_tma_enabled() && ldd % 4 == 0 &&
+      (reinterpret_cast<uintptr_t>(D) & 15) == 0) {
+    uint64_t dims[2] = {(uint64_t)N, (uint64_t)M};
+    uint64_t strides[1] = {(uint64_t)ldd * 4};
+    uint32_t box[2] = {32, 32};
+    if (int rc = get_map(&pm.m[0], D, 2, dims, strides, box, true)) return rc;
+    pm.add_tma = 1;
+  }
   if (t_peer_ptrs_host != nullptr && p.peer_ptrs != nullptr && epilogue == SP_EPI_STORE_BF16 &&
       peer_width % 64 == 0 && N / peer_width <= kMaxPeerMaps && peer_tma_enabled()) {
     // one store map per peer over the rows this pass owns in it
@@ -1438,7 +1511,7 @@ static int launch_pair(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
     }
     pm.n = np;
   }
-  const int smem = pm.n > 0 ? pair::SMEM_BYTES_TMA : pair::SMEM_BYTES;
+  const int smem = (pm.n > 0 || pm.add_tma) ? pair::SMEM_BYTES_TMA : pair::SMEM_BYTES;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -443,6 +443,27 @@ def test_gemm_cta_pair_large_tiles(epi, monkeypatch):
     assert torch.equal(outs["1"], outs["0"])
 
 
+@pytest.mark.parametrize("M,ldd", [(1000, 4096), (777, 4352), (8192, 4096)])
+def test_gemm_pair_residual_add_tma_bitexact(M, ldd, monkeypatch):
+    """The pair kernel's residual add through TMA boxes (SP_ADD_TMA, default on)
+    is bit-identical to the direct per-row read-modify-write, on ragged row
+    counts (OOB rows of the last box neither read nor written) and on a
+    residual with a row stride wider than N (columns past N untouched)."""
+    N, K = 4096, 1024
+    a, b = rnd(M, K, seed=52), rnd(N, K, seed=53)
+    base = torch.randn(M, ldd, device="cuda", generator=torch.Generator("cuda").manual_seed(54))
+    outs = {}
+    for on in ("1", "0"):
+        monkeypatch.setenv("SP_ADD_TMA", on)
+        d = base.clone()
+        ops.gemm(a, b, d, ops.EPI_ADD_F32, M=M, N=N, K=K, lda=K, ldb=K, ldd=ldd)
+        torch.cuda.synchronize()
+        assert torch.equal(d[:, N:], base[:, N:])
+        assert rel(d[:, :N], base[:, :N] + a.float() @ b.float().t()) < 1e-4
+        outs[on] = d
+    assert torch.equal(outs["1"], outs["0"])
+
+
 @pytest.mark.parametrize("M,N,K", [(64, 4096, 4096), (1, 4096, 14336), (100, 1024, 4096),
                                    (200, 4096, 4096), (300, 512, 1024)])
 def test_gemm_partials_fused_into_rmsnorm_bitexact(M, N, K):
