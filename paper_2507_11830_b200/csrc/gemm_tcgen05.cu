@@ -103,11 +103,20 @@ struct PeerMaps {
   // box, adds the accumulator in shared memory and TMA-stores it back — whole
   // 128-B lines per instruction instead of 32 row-strided lines per warp access
   int add_tma;
+  // bf16 outputs (STORE_BF16 / GELU / SWIGLU) through TMA: m[0] is a bf16 map
+  // of D, box 64 x 32 with 128-B swizzle; each warp packs 32 rows x 64 columns
+  // into a staging box (two per warp, alternating) and one TMA store writes it
+  int store_tma;
 };
 static thread_local const unsigned long long* t_peer_ptrs_host = nullptr;
 
 static bool add_tma_enabled() {  // SP_ADD_TMA=0: direct residual-add stores (A/B runs)
   const char* e = getenv("SP_ADD_TMA");
+  return !(e && e[0] == '0');
+}
+
+static bool store_tma_enabled() {  // SP_STORE_TMA=0: direct bf16 epilogue stores (A/B runs)
+  const char* e = getenv("SP_STORE_TMA");
   return !(e && e[0] == '0');
 }
 
@@ -981,6 +990,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const int m = mb * 256 + rank * 128 + row;
       if (p.epi == EPI_QKV_ROPE) {
         qkv_rope_row(p, m, nb * 256, tb);
+      } else if (pm.store_tma) {
+        uint8_t* stage = smem + pair::OUT_OFF + quarter * 8192;
+        const int mrow0 = mb * 256 + rank * 128 + quarter * 32;
+        const bool swiglu = p.epi == SP_EPI_SWIGLU;
+        const int out_cols = swiglu ? 128 : 256;
+#pragma unroll 1
+        for (int c = 0; c < out_cols; c += 64) {
+          uint32_t r0[32], r1[32];
+          float v[64];
+          if (swiglu) {
+            uint32_t u0[32], u1[32];
+            tmem_ld32(tb + c, r0);
+            tmem_ld32(tb + c + 32, r1);
+            tmem_ld32(tb + 128 + c, u0);
+            tmem_ld32(tb + 128 + c + 32, u1);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              v[j] = silu(__uint_as_float(r0[j])) * __uint_as_float(u0[j]);
+              v[32 + j] = silu(__uint_as_float(r1[j])) * __uint_as_float(u1[j]);
+            }
+          } else {
+            tmem_ld32(tb + c, r0);
+            tmem_ld32(tb + c + 32, r1);
+            tmem_ld_wait();
+            const bool gelu = p.epi == SP_EPI_GELU;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float x0 = __uint_as_float(r0[j]), x1 = __uint_as_float(r1[j]);
+              v[j] = gelu ? gelu_tanh(x0) : x0;
+              v[32 + j] = gelu ? gelu_tanh(x1) : x1;
+            }
+          }
+          uint8_t* box = stage + ((c >> 6) & 1) * 4096;
+          if (lane == 0) bulk_wait_read1();  // this buffer's store two boxes back has left smem
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint4 u;
+            u.x = pack_bf16x2(v[8 * j + 0], v[8 * j + 1]);
+            u.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
+            u.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
+            u.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
+            *reinterpret_cast<uint4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) = u;
+          }
+          fence_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&pm.m[0], box, nb * out_cols + c, mrow0);
+            bulk_commit();
+          }
+        }
       } else if (p.epi == SP_EPI_SWIGLU) {
 #pragma unroll 1
         for (int c = 0; c < 128; c += 32) {
@@ -1100,7 +1161,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
     }
   }
-  if ((pm.n > 0 || pm.add_tma) && warp >= 2 && (threadIdx.x & 31) == 0)
+  if ((pm.n > 0 || pm.add_tma || pm.store_tma) && warp >= 2 && (threadIdx.x & 31) == 0)
     bulk_wait0();  // stores landed
   tc_fence_before();
   pair::cluster_sync();
@@ -1489,6 +1550,7 @@ static int launch_pair(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
   PeerMaps pm;
   pm.n = 0;
   pm.add_tma = 0;
+  pm.store_tma = 0;
   if (epilogue == SP_EPI_ADD_F32 && peer_width == 0 && add_tma_enabled() && ldd % 4 == 0 &&
       (reinterpret_cast<uintptr_t>(D) & 15) == 0) {
     uint64_t dims[2] = {(uint64_t)N, (uint64_t)M};
@@ -1496,6 +1558,16 @@ static int launch_pair(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
     uint32_t box[2] = {32, 32};
     if (int rc = get_map(&pm.m[0], D, 2, dims, strides, box, true)) return rc;
     pm.add_tma = 1;
+  }
+  if ((epilogue == SP_EPI_STORE_BF16 || epilogue == SP_EPI_GELU || epilogue == SP_EPI_SWIGLU) &&
+      peer_width == 0 && store_tma_enabled() && ldd % 8 == 0 &&
+      (reinterpret_cast<uintptr_t>(D) & 15) == 0) {
+    const int out_cols = epilogue == SP_EPI_SWIGLU ? N / 2 : N;
+    uint64_t dims[2] = {(uint64_t)out_cols, (uint64_t)M};
+    uint64_t strides[1] = {(uint64_t)ldd * 2};
+    uint32_t box[2] = {64, 32};
+    if (int rc = get_map(&pm.m[0], D, 2, dims, strides, box)) return rc;
+    pm.store_tma = 1;
   }
   if (t_peer_ptrs_host != nullptr && p.peer_ptrs != nullptr && epilogue == SP_EPI_STORE_BF16 &&
       peer_width % 64 == 0 && N / peer_width <= kMaxPeerMaps && peer_tma_enabled()) {
@@ -1511,7 +1583,7 @@ static int launch_pair(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
     }
     pm.n = np;
   }
-  const int smem = (pm.n > 0 || pm.add_tma) ? pair::SMEM_BYTES_TMA : pair::SMEM_BYTES;
+  const int smem = (pm.n > 0 || pm.add_tma || pm.store_tma) ? pair::SMEM_BYTES_TMA : pair::SMEM_BYTES;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -464,6 +464,34 @@ def test_gemm_pair_residual_add_tma_bitexact(M, ldd, monkeypatch):
     assert torch.equal(outs["1"], outs["0"])
 
 
+@pytest.mark.parametrize("epi", ["bf16", "swiglu", "gelu"])
+@pytest.mark.parametrize("M,pad", [(1000, 0), (777, 64), (4096, 0)])
+def test_gemm_pair_bf16_store_tma_bitexact(epi, M, pad, monkeypatch):
+    """bf16 epilogues of the pair kernel through TMA boxes (SP_STORE_TMA,
+    default on) are bit-identical to the direct row stores, on ragged rows and
+    on an output with a row stride wider than its columns (padding untouched)."""
+    N, K = 4096, 1024
+    a, b = rnd(M, K, seed=55), rnd(N, K, seed=56)
+    code = {"bf16": ops.EPI_STORE_BF16, "swiglu": ops.EPI_SWIGLU, "gelu": ops.EPI_GELU}[epi]
+    cols = N // 2 if epi == "swiglu" else N
+    outs = {}
+    for on in ("1", "0"):
+        monkeypatch.setenv("SP_STORE_TMA", on)
+        d = torch.full((M, cols + pad), 7.0, device="cuda", dtype=torch.bfloat16)
+        ops.gemm(a, b, d, code, M=M, N=N, K=K, lda=K, ldb=K, ldd=cols + pad)
+        torch.cuda.synchronize()
+        assert bool((d[:, cols:] == 7.0).all())
+        outs[on] = d
+    ref = a.float() @ b.float().t()
+    if epi == "swiglu":
+        v = ref.view(M, N // 256, 2, 128)
+        ref = (torch.nn.functional.silu(v[:, :, 0]) * v[:, :, 1]).reshape(M, cols)
+    elif epi == "gelu":
+        ref = torch.nn.functional.gelu(ref, approximate="tanh")
+    assert rel(outs["1"][:, :cols], ref) < 1e-2
+    assert torch.equal(outs["1"], outs["0"])
+
+
 @pytest.mark.parametrize("M,N,K", [(64, 4096, 4096), (1, 4096, 14336), (100, 1024, 4096),
                                    (200, 4096, 4096), (300, 512, 1024)])
 def test_gemm_partials_fused_into_rmsnorm_bitexact(M, N, K):

@@ -3,6 +3,7 @@ epilogues (graph-replayed back to back, L2 flushed between graphs), TFLOP/s.
 
     python tools/epi_probe.py             # every epilogue per shape
     python tools/epi_probe.py addtma      # interleaved A/B of the TMA residual-add epilogue
+    python tools/epi_probe.py storetma    # interleaved A/B of the TMA bf16-store epilogue
 """
 import os
 import sys
@@ -51,6 +52,14 @@ if len(sys.argv) > 1 and sys.argv[1] == "addtma":  # A/B of the TMA residual add
             for on in ("0", "1"):
                 os.environ["SP_ADD_TMA"] = on
                 bench(N, K, ops.EPI_ADD_F32, f"{name} add_f32 add_tma={on}")
+    sys.exit(0)
+if len(sys.argv) > 1 and sys.argv[1] == "storetma":  # A/B of the TMA bf16 store, interleaved
+    for rep in range(3):
+        for N, K, name, epi in ((28672, 4096, "gate_up swiglu", ops.EPI_SWIGLU),
+                                (6144, 4096, "QKV bf16", ops.EPI_STORE_BF16)):
+            for on in ("0", "1"):
+                os.environ["SP_STORE_TMA"] = on
+                bench(N, K, epi, f"{name} store_tma={on}")
     sys.exit(0)
 for N, K, name in ((4096, 4096, "O"), (4096, 14336, "down"), (6144, 4096, "QKV"), (28672, 4096, "gate_up")):
     for epi, en in ((ops.EPI_STORE_BF16, "bf16"), (ops.EPI_STORE_F32, "f32"), (ops.EPI_ADD_F32, "add_f32"),
