@@ -208,6 +208,63 @@ __device__ __forceinline__ void qkv_rope_row(const Params& p, int m, int n0, uin
   }
 }
 
+// EPI_QKV_ROPE for a tile of two query heads through TMA: the warp's 32 rows
+// of each head are rotated exactly as qkv_rope_row does, packed into two
+// 128-B-swizzled boxes (head columns [0, 64) and [64, 128)) and TMA-stored
+// into q_out with the map `qmap` (rows past M are clipped by the map)
+__device__ __forceinline__ void qkv_rope_q_tma(const Params& p, const CUtensorMap* qmap, int m,
+                                               int n0, uint32_t tb, uint8_t* stage, int lane,
+                                               int mrow0) {
+  const Params::Rope& R = p.rope;
+  const int pos = m < p.M ? R.pos[m] : 0;
+  const bool rotate = R.table != nullptr;
+#pragma unroll 1
+  for (int hh = 0; hh < 2; ++hh) {
+    const int h = (n0 >> 7) + hh;
+    if (lane == 0) bulk_wait_read0();  // both boxes of the previous head have left smem
+    __syncwarp();
+#pragma unroll 1
+    for (int c = 0; c < 64; c += 32) {
+      uint32_t ra[32], rb[32];
+      tmem_ld32(tb + hh * 128 + c, ra);
+      tmem_ld32(tb + hh * 128 + 64 + c, rb);
+      tmem_ld_wait();
+      uint32_t oa[16], ob[16];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const float2 a = unpack_bf16x2(pack_bf16x2(__uint_as_float(ra[j]), __uint_as_float(ra[j + 1])));
+        const float2 b = unpack_bf16x2(pack_bf16x2(__uint_as_float(rb[j]), __uint_as_float(rb[j + 1])));
+        if (rotate) {
+          const float4 cs = *reinterpret_cast<const float4*>(R.table + ((int64_t)pos * 64 + c + j) * 2);
+          float na0, nb0, na1, nb1;
+          rope_rotate(a.x, b.x, cs.x, cs.y, na0, nb0);
+          rope_rotate(a.y, b.y, cs.z, cs.w, na1, nb1);
+          oa[j / 2] = pack_bf16x2(na0, na1);
+          ob[j / 2] = pack_bf16x2(nb0, nb1);
+        } else {
+          oa[j / 2] = pack_bf16x2(a.x, a.y);
+          ob[j / 2] = pack_bf16x2(b.x, b.y);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = (c >> 3) + q;  // 16-B chunk index inside the 128-B box row
+        const uint32_t off = lane * 128 + ((j ^ (lane & 7)) << 4);
+        *reinterpret_cast<uint4*>(stage + off) = make_uint4(oa[4 * q], oa[4 * q + 1], oa[4 * q + 2], oa[4 * q + 3]);
+        *reinterpret_cast<uint4*>(stage + 4096 + off) =
+            make_uint4(ob[4 * q], ob[4 * q + 1], ob[4 * q + 2], ob[4 * q + 3]);
+      }
+    }
+    fence_async_shared();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(qmap, stage, h * 128, mrow0);
+      tma_store_2d(qmap, stage + 4096, h * 128 + 64, mrow0);
+      bulk_commit();
+    }
+  }
+}
+
 __device__ __forceinline__ void tile_coords(int t, const Params& p, int& mb, int& nb) {
   if (p.group_n > 0) {  // B-resident raster: a group of N tiles sweeps every M tile
     const int per_group = p.group_n * p.num_m;
@@ -989,7 +1046,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const uint32_t tb = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * 256;
       const int m = mb * 256 + rank * 128 + row;
       if (p.epi == EPI_QKV_ROPE) {
-        qkv_rope_row(p, m, nb * 256, tb);
+        if (pm.store_tma && nb * 2 + 1 < p.rope.q_heads)
+          qkv_rope_q_tma(p, &pm.m[0], m, nb * 256, tb, smem + pair::OUT_OFF + quarter * 8192, lane,
+                         mb * 256 + rank * 128 + quarter * 32);
+        else
+          qkv_rope_row(p, m, nb * 256, tb);
       } else if (pm.store_tma) {
         uint8_t* stage = smem + pair::OUT_OFF + quarter * 8192;
         const int mrow0 = mb * 256 + rank * 128 + quarter * 32;
@@ -1567,6 +1628,14 @@ static int launch_pair(const void* A, int64_t lda, int64_t a_kchunk, int64_t a_c
     uint64_t strides[1] = {(uint64_t)ldd * 2};
     uint32_t box[2] = {64, 32};
     if (int rc = get_map(&pm.m[0], D, 2, dims, strides, box)) return rc;
+    pm.store_tma = 1;
+  }
+  if (epilogue == EPI_QKV_ROPE && p.rope.q_out != nullptr && store_tma_enabled() &&
+      p.rope.ldq % 8 == 0 && (reinterpret_cast<uintptr_t>(p.rope.q_out) & 15) == 0) {
+    uint64_t dims[2] = {(uint64_t)p.rope.q_heads * 128, (uint64_t)M};
+    uint64_t strides[1] = {(uint64_t)p.rope.ldq * 2};
+    uint32_t box[2] = {64, 32};
+    if (int rc = get_map(&pm.m[0], p.rope.q_out, 2, dims, strides, box)) return rc;
     pm.store_tma = 1;
   }
   if (t_peer_ptrs_host != nullptr && p.peer_ptrs != nullptr && epilogue == SP_EPI_STORE_BF16 &&
