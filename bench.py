@@ -496,10 +496,12 @@ def run_ours(args):
                 * cfg.head_dim * 2
             row = {}
             for mode in (ParallelMode.TP, ParallelMode.SP):
-                for _ in range(3):  # eager, capture, replay
+                # eager, capture, then replays until the TPOT is steady (the
+                # first replays after a prefill-heavy phase run ~5% slow)
+                for _ in range(12):
                     dstep(mode)
                     roll_back()
-                n_dec = 16
+                n_dec = 32
 
                 def one():
                     dstep(mode)
