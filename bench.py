@@ -83,7 +83,7 @@ def workload_config(args, world: int) -> dict:
 def traffic_per_launch(kernel: str):
     """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
     capture of this workload (tools/ncu_traffic.py)."""
-    for name in ("r02_traffic.json", "r01_traffic.json"):
+    for name in ("r02_traffic_final.json", "r02_traffic.json", "r01_traffic.json"):
         try:
             with open(os.path.join(ROOT, "profiles", name)) as f:
                 return round(json.load(f)["kernels"][kernel]["dram_bytes_per_launch"])
