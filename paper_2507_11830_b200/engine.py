@@ -544,7 +544,7 @@ class Engine:
         spans = [len(it.tokens) for it in items]
         hist = [it.seq.cache.token_count for it in items]
         M = sum(spans)
-        toks = np.fromiter((t for it in items for t in it.tokens), dtype=np.int32, count=M)
+        toks = np.concatenate([np.asarray(it.tokens, dtype=np.int32) for it in items])
         pos = np.concatenate([np.arange(h0, h0 + m, dtype=np.int32) for h0, m in zip(hist, spans)])
         slots = np.concatenate([alloc.slots(it.seq.cache.key, h0, m)
                                 for it, h0, m in zip(items, hist, spans)])
