@@ -836,7 +836,10 @@ __global__ void __launch_bounds__(NUM_THREADS, SwapTile<NT>::CTAS_PER_SM)
 // both CTAs' operands and writes each CTA's 128 accumulator rows into its own
 // TMEM.  Per SM this halves the B bytes staged per FLOP vs the 1-CTA kernel.
 namespace pair {
-constexpr int STAGES = 6;
+#ifndef PAIR_STAGES
+#define PAIR_STAGES 6
+#endif
+constexpr int STAGES = PAIR_STAGES;
 constexpr int A_BYTES = 128 * BK * 2;
 constexpr int B_BYTES = 128 * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;

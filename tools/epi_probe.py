@@ -4,6 +4,7 @@ epilogues (graph-replayed back to back, L2 flushed between graphs), TFLOP/s.
     python tools/epi_probe.py             # every epilogue per shape
     python tools/epi_probe.py addtma      # interleaved A/B of the TMA residual-add epilogue
     python tools/epi_probe.py storetma    # interleaved A/B of the TMA bf16-store epilogue
+    python tools/epi_probe.py prod [tag]  # the four prefill projections with their production epilogues
     python tools/epi_probe.py qkvtma      # interleaved A/B of the TMA q store (QKV + RoPE epilogue)
 """
 import os
@@ -91,6 +92,13 @@ def bench_qkv_rope(label, reps=5, n_in=4, hq=32, hk=8, K=4096, bs=64):
     print(f"{label:28s} N={N:6d} K={K:6d} {ms * 1e3:8.1f} us  {2 * M * N * K / ms / 1e9:7.1f} TFLOP/s", flush=True)
 
 
+if len(sys.argv) > 1 and sys.argv[1] == "prod":  # the four prefill projections as the engine runs them
+    tag = sys.argv[2] if len(sys.argv) > 2 else ""
+    bench_qkv_rope(f"{tag} QKV rope")
+    bench(4096, 4096, ops.EPI_ADD_F32, f"{tag} O add_f32")
+    bench(28672, 4096, ops.EPI_SWIGLU, f"{tag} gate_up swiglu")
+    bench(4096, 14336, ops.EPI_ADD_F32, f"{tag} down add_f32")
+    sys.exit(0)
 if len(sys.argv) > 1 and sys.argv[1] == "qkvtma":  # A/B of the TMA q store in the QKV+RoPE epilogue
     for rep in range(3):
         for on in ("0", "1"):
