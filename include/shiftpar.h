@@ -56,6 +56,12 @@ int sp_abi_version(void);
 int64_t sp_kernel_launches(void);
 /* 0 when the current device is sm_100 (B200) and the kernels can run. */
 sp_status sp_device_check(int* sm_count);
+/* Debug builds (-DSTEP_TRACE) only: bind a device buffer of `cap` 32-byte
+ * records {tag, t_entry, t_wait, t_exit} and a uint32 record counter; every
+ * CTA of every kernel then appends its globaltimer stamps (tools/step_trace.py).
+ * Returns SP_UNSUPPORTED (3) in production builds.  No reference counterpart:
+ * instrumentation of the B200 kernel chain. */
+sp_status sp_step_trace_bind(void* buf, void* counter, int cap);
 
 /* --------------------------------------------------------------- GEMM
  * Replaces tensor_core.matmul (tensor_core.py:75-102) for every projection:

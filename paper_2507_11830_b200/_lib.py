@@ -26,6 +26,7 @@ SIGNATURES = {
     "sp_abi_version": (_c_int, []),
     "sp_kernel_launches": (_i64, []),
     "sp_device_check": (_c_int, [ctypes.POINTER(_c_int)]),
+    "sp_step_trace_bind": (_c_int, [_vp, _vp, _c_int]),
     "sp_gemm_bf16": (_c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _c_int, _c_int, _c_int,
                               _c_int, _i64, _i64, _vp]),
     "sp_gemm_set_workspace": (_c_int, [_vp, _i64]),

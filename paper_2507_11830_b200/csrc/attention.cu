@@ -18,6 +18,7 @@
 #include "../../include/shiftpar.h"
 #include <cstring>
 
+#define SP_TU_ID 1  // step-trace tag (common.cuh)
 #include "common.cuh"
 
 namespace sp {

@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 
 #include "../../include/shiftpar.h"
+#define SP_TU_ID 2  // step-trace tag (common.cuh)
 #include "common.cuh"
 
 namespace sp {

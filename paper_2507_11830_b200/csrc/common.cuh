@@ -33,10 +33,82 @@ enum Status : int {
 // can launch early.  Disabled with SP_PDL=0.
 bool pdl_enabled();
 
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() {
+__device__ __forceinline__ void pdl_wait_impl() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger_impl() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+
+// ------------------------------------------------ step timeline (debug builds)
+// Built with -DSTEP_TRACE (tools/step_trace.py): every CTA of every kernel
+// records the call site of its entry pdl_trigger() (translation unit, line),
+// its block, and globaltimer stamps at entry, at griddepcontrol.wait release
+// and at exit into a device buffer the host binds with sp_step_trace_bind.
+// The production build compiles none of it.
+struct StepTraceRec {
+  unsigned long long tag;  // [63:32] linear block index, [31:16] TU id, [15:0] line
+  unsigned long long t_entry, t_wait, t_exit;
+};
+void step_trace_register(void (*bind)(void* buf, void* counter, int cap));
+
+#ifndef SP_TU_ID
+#define SP_TU_ID 0
+#endif
+
+#ifdef STEP_TRACE
+__device__ __forceinline__ unsigned long long sp_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+static __device__ StepTraceRec* g_st_buf = nullptr;
+static __device__ unsigned int* g_st_n = nullptr;
+static __device__ int g_st_cap = 0;
+static __shared__ unsigned int sp_st_slot;
+
+struct StepTraceScope {
+  __device__ explicit StepTraceScope(unsigned tag) {
+    if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0) {
+      unsigned s = ~0u;
+      if (g_st_buf != nullptr) s = atomicAdd(g_st_n, 1u);
+      sp_st_slot = s;
+      if (s < (unsigned)g_st_cap) {
+        const unsigned long long blk = blockIdx.x + (unsigned long long)blockIdx.y * gridDim.x +
+                                       (unsigned long long)blockIdx.z * gridDim.x * gridDim.y;
+        g_st_buf[s].tag = (blk << 32) | tag;
+        g_st_buf[s].t_wait = 0;
+        g_st_buf[s].t_entry = sp_gtime();
+      }
+    }
+    __syncwarp();
+  }
+  __device__ ~StepTraceScope() {
+    if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0) {
+      const unsigned s = sp_st_slot;
+      if (s < (unsigned)g_st_cap) g_st_buf[s].t_exit = sp_gtime();
+    }
+  }
+};
+__device__ __forceinline__ void sp_trace_wait() {
+  if ((threadIdx.x & 31) == 0 && g_st_buf != nullptr) {
+    const unsigned s = sp_st_slot;
+    if (s < (unsigned)g_st_cap) atomicCAS(&g_st_buf[s].t_wait, 0ull, sp_gtime());
+  }
+}
+#define pdl_trigger()                                                                \
+  ::sp::StepTraceScope sp_step_trace_scope_((SP_TU_ID << 16) | (__LINE__ & 0xffff)); \
+  ::sp::pdl_trigger_impl()
+#define pdl_wait() (::sp::pdl_wait_impl(), ::sp::sp_trace_wait())
+// binds this translation unit's trace pointers (registered at load time)
+static void step_trace_bind_local(void* buf, void* counter, int cap) {
+  cudaMemcpyToSymbol(g_st_buf, &buf, sizeof(buf));
+  cudaMemcpyToSymbol(g_st_n, &counter, sizeof(counter));
+  cudaMemcpyToSymbol(g_st_cap, &cap, sizeof(cap));
+}
+static const bool sp_step_trace_registered_ = (step_trace_register(step_trace_bind_local), true);
+#else
+#define pdl_trigger() ::sp::pdl_trigger_impl()
+#define pdl_wait() ::sp::pdl_wait_impl()
+#endif
 
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,

@@ -41,6 +41,7 @@
 #include <string>
 
 #include "../../include/shiftpar.h"
+#define SP_TU_ID 3  // step-trace tag (common.cuh)
 #include "common.cuh"
 
 namespace sp {
@@ -547,7 +548,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) decode_layer_kernel(const __gr
         const int need = a.proj[p].need;
         if (need == 0) {
           if (!block) return false;
-          pdl_wait();
+          pdl_wait_impl();
           tr(2);
         } else {
           if (ld_acquire_cta(bars_done) < (unsigned)need) return false;
@@ -640,7 +641,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) decode_layer_kernel(const __gr
     const int etid = threadIdx.x - 64;
     const int quarter = warp & 3;  // TMEM lanes this warp may read
     const int nl = quarter * 32 + lane;
-    pdl_wait();  // x, the input rows and the pool are written by predecessors
+    pdl_wait_impl();  // x, the input rows and the pool are written by predecessors
     unsigned bars = 0;
     int acc = 0;
     uint32_t aphase = 0;
@@ -653,7 +654,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) decode_layer_kernel(const __gr
       grid_barrier(a.sync, bars, (unsigned)G, etid, bars_done);
       if (etid == 0) tr(19 + 2 * (int)bars);
       if (!triggered) {  // every CTA is resident now: successors may launch
-        pdl_trigger();
+        pdl_trigger_impl();
         triggered = true;
       }
     };
@@ -710,7 +711,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) decode_layer_kernel(const __gr
       }
       if (p + 1 < a.n_proj) barrier();  // the next projection's input rows are out
     }
-    if (!triggered) pdl_trigger();
+    if (!triggered) pdl_trigger_impl();
   }
   __syncthreads();
   if (warp == 1) {

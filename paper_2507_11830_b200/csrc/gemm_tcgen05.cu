@@ -25,6 +25,7 @@
 #include <cstdio>
 
 #include "../../include/shiftpar.h"
+#define SP_TU_ID 4  // step-trace tag (common.cuh)
 #include "common.cuh"
 
 namespace sp {
@@ -850,7 +851,11 @@ constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int OUT_OFF = STAGES * STAGE_BYTES + 1024;  // past the barriers, 1024-aligned
 constexpr int OUT_BYTES = 8 * 4096;
 constexpr int OUT_BAR_OFF = OUT_OFF + OUT_BYTES;      // 8 box-load barriers (residual add)
+#ifdef STEP_TRACE  // the trace slot's static shared word (1 KiB-aligned) leaves less dynamic room
+constexpr int SMEM_BYTES_TMA = OUT_BAR_OFF + 64 + 896;
+#else
 constexpr int SMEM_BYTES_TMA = OUT_BAR_OFF + 64 + 1024;
+#endif
 static_assert(SMEM_BYTES_TMA <= 232448, "pair TMA-epilogue smem over the 227 KiB limit");
 
 __device__ __forceinline__ uint32_t cta_rank() {

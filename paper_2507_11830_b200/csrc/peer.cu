@@ -12,6 +12,7 @@
 #include <string>
 
 #include "../../include/shiftpar.h"
+#define SP_TU_ID 5  // step-trace tag (common.cuh)
 #include "common.cuh"
 
 namespace sp {

@@ -6,8 +6,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "../../include/shiftpar.h"
+#define SP_TU_ID 6  // step-trace tag (common.cuh)
 #include "common.cuh"
 
 namespace sp {
@@ -30,6 +32,15 @@ bool pdl_enabled() {
     on = (e && e[0] == '0') ? 0 : 1;
   }
   return on == 1;
+}
+
+static std::vector<void (*)(void*, void*, int)>& step_trace_registry() {
+  static std::vector<void (*)(void*, void*, int)> v;
+  return v;
+}
+
+void step_trace_register(void (*bind)(void* buf, void* counter, int cap)) {
+  step_trace_registry().push_back(bind);
 }
 
 bool l2_hint_enabled() {
@@ -689,3 +700,21 @@ extern "C" sp_status sp_gather_rows_bf16(const void* src, int64_t lds, const int
   return check_launch("gather_rows_u16_kernel");
 }
 
+// Step timeline (debug builds only, see common.cuh): bind the record buffer
+// (StepTraceRec[cap], 32 B each) and its 32-bit record counter in every
+// translation unit; cap 0 / NULL buffer unbinds.
+extern "C" sp_status sp_step_trace_bind(void* buf, void* counter, int cap) {
+#ifdef STEP_TRACE
+  if (cap < 0 || (cap > 0 && (buf == nullptr || counter == nullptr)))
+    return sp::fail(sp::kInvalid, "step_trace_bind: buffer, counter and cap >= 0 required");
+  for (auto f : sp::step_trace_registry()) f(cap > 0 ? buf : nullptr, counter, cap);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return sp::fail(sp::kCuda, std::string("step_trace_bind: ") + cudaGetErrorString(e));
+  return sp::kOk;
+#else
+  (void)buf;
+  (void)counter;
+  (void)cap;
+  return sp::fail(sp::kUnsupported, "step_trace_bind: library built without -DSTEP_TRACE");
+#endif
+}

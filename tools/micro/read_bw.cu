@@ -138,6 +138,32 @@ int main() {
              c.stages, c.stage, us, (double)per * c.ctas / (us * 1e-6) / 1e9);
     }
   }
+  // decode-attention-sized streams: B=64 x 8 kv heads x ctx 2048 = 512 (item,
+  // head) pairs of 1 MiB K+V each (537 MB per launch), rotating over 3 slices
+  {
+    const size_t slice = (size_t)512 << 20;
+    struct Sh { int ctas, stage, stages, smem_pad; };
+    const Sh shs[] = {{512, 32768, 3, 0}, {512, 32768, 3, 100000}, {512, 16384, 3, 0},
+                      {1024, 32768, 3, 0}, {296, 32768, 3, 0}, {592, 32768, 3, 0}};
+    for (const Sh& c : shs) {
+      size_t per = slice / c.ctas / c.stage * c.stage;
+      const int smem = c.stage * c.stages + 64 * 8 + c.smem_pad;
+      cudaFuncSetAttribute(bulk_read<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      for (int w = 0; w < 3; ++w)
+        bulk_read<true><<<c.ctas, 32, smem>>>(buf + (size_t)w * slice, per, c.stage, c.stages, sink);
+      cudaEventRecord(e0);
+      const int reps = 30;
+      for (int r = 0; r < reps; ++r)
+        bulk_read<true><<<c.ctas, 32, smem>>>(buf + (size_t)(r % 3) * slice, per, c.stage, c.stages, sink);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double us = ms * 1e3 / reps;
+      printf("512MB %4d CTAs x %7zu B (ring %d x %d, smem %d): %6.1f us/launch  %7.1f GB/s\n", c.ctas, per,
+             c.stages, c.stage, smem, us, (double)per * c.ctas / (us * 1e-6) / 1e9);
+    }
+  }
   for (int tpb : {256, 512, 1024}) {
     for (int bps : {1, 2, 4, 8}) {
       if (tpb * bps > 2048) continue;

@@ -50,8 +50,39 @@ eng.step(Batch(BatchKind.PREFILL, [BatchItem(seq, prompt)]), mode=ParallelMode.S
 e1.record()
 torch.cuda.synchronize()
 print(f"device time of one step {e0.elapsed_time(e1):.2f} ms")
+e0.record()
+for _ in range(3):
+    seq.cache.truncate(0)
+    eng.step(Batch(BatchKind.PREFILL, [BatchItem(seq, prompt)]), mode=ParallelMode.SP)
+e1.record()
+torch.cuda.synchronize()
+print(f"device time per step, 3 back to back {e0.elapsed_time(e1) / 3:.2f} ms")
+# host time from step() entry to the first kernel launch (the embedding)
+from paper_2507_11830_b200 import ops  # noqa: E402
+stamp = {}
+_embed = ops.embed
+
+
+def embed_stamp(*a, **k):
+    stamp.setdefault("t", time.perf_counter())
+    return _embed(*a, **k)
+
+
+ops.embed = embed_stamp
+import paper_2507_11830_b200.engine as engmod  # noqa: E402
+engmod.ops.embed = embed_stamp
+for _ in range(3):
+    stamp.clear()
+    torch.cuda.synchronize()
+    seq.cache.truncate(0)
+    t0 = time.perf_counter()
+    eng.step(Batch(BatchKind.PREFILL, [BatchItem(seq, prompt)]), mode=ParallelMode.SP)
+    print(f"step() entry -> first launch {(stamp['t'] - t0) * 1e3:.3f} ms")
+torch.cuda.synchronize()
+ops.embed = _embed
+engmod.ops.embed = _embed
 pr = cProfile.Profile()
 pr.enable()
 one()
 pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(14)
+pstats.Stats(pr).sort_stats("cumulative").print_stats(40)
