@@ -66,7 +66,7 @@ def decode_sweep(weights, cfg, ctx=2048, tau=32):
                 for s in sub:
                     s.cache.truncate(s.cache.token_count - 1)
             before = sum(s.cache.write_counter for s in sub)
-            res[label] = timed(step, 8)
+            res[label] = timed(step, 24, warm=12)  # first replays after a capture run slow
             chosen = eng.mode_log[-1].value
         kv_bytes = B * ctx * cfg.n_layers * 2 * cfg.kv_heads * cfg.head_dim * 2
         roof = (wbytes + kv_bytes) / (PEAKS["hbm_gbs"] * 1e9) * 1e3
