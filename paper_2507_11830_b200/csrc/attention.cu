@@ -422,18 +422,33 @@ __global__ void combine_kernel(Params p, int head_dim) {
   pdl_trigger();  // successors may launch now: they wait for this grid before reading its outputs
   pdl_wait();  // inputs of this kernel are written by its predecessor
   const int item = blockIdx.x, qh = blockIdx.y;
-  const int64_t base = ((int64_t)item * p.q_heads + qh) * p.n_splits;
-  float mx = -INFINITY;
-  for (int s = 0; s < p.n_splits; ++s) mx = fmaxf(mx, p.ws_lse[base + s]);
+  const int ns = p.n_splits;  // <= 64 (decode_tma_splits)
+  const int64_t base = ((int64_t)item * p.q_heads + qh) * ns;
+  // every split's log-sum-exp in one round trip, then the partial rows with
+  // 8 loads in flight per thread; the arithmetic (max, then ascending-split
+  // weights and sums) is the sequential fold, so results do not change
+  __shared__ float lse[64];
+  for (int s = threadIdx.x; s < ns; s += blockDim.x) lse[s] = p.ws_lse[base + s];
   const int q_row = p.cu_q[item];
+  __syncthreads();
+  float mx = -INFINITY;
+  for (int s = 0; s < ns; ++s) mx = fmaxf(mx, lse[s]);
   for (int c = threadIdx.x; c < head_dim; c += blockDim.x) {
     float w = 0.f, acc = 0.f;
-    for (int s = 0; s < p.n_splits; ++s) {
-      const float l = p.ws_lse[base + s];
-      if (l == -INFINITY) continue;
-      const float f = exp2f(l - mx);
-      w += f;
-      acc += f * p.ws_o[(base + s) * head_dim + c];
+    for (int s0 = 0; s0 < ns; s0 += 8) {
+      float o[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        o[u] = s0 + u < ns && lse[s0 + u] != -INFINITY ? p.ws_o[(base + s0 + u) * head_dim + c] : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (s0 + u >= ns) break;
+        const float l = lse[s0 + u];
+        if (l == -INFINITY) continue;
+        const float f = exp2f(l - mx);
+        w += f;
+        acc += f * o[u];
+      }
     }
     p.out[(int64_t)q_row * p.ldo + (int64_t)qh * head_dim + c] = __float2bfloat16_rn(acc / w);
   }
