@@ -4,9 +4,11 @@
 // way the swap-AB decode GEMM's producer streams weight boxes, optionally with
 // the L2 evict-first hint; the consumer thread only re-arms the stage.  Also
 // an LDG.128 read kernel (all threads, sum folded into one store).
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o read_bw read_bw.cu && ./read_bw
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o read_bw read_bw.cu -lcuda && ./read_bw
 #include <cstdio>
 #include <cstdint>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -57,6 +59,56 @@ __global__ void bulk_read(const uint8_t* src, size_t bytes_per_cta, int stage_by
     phase[s] ^= 1;
     acc += smem[(size_t)s * stage_bytes];
     if (i + stages < n) issue(i + stages);
+  }
+  if (acc == 0xdeadbeef) *sink = acc;
+}
+
+// The decode attention's pattern: per 64-key page slice, four 2-D tensor-map
+// boxes of [64 rows][64 bf16] (128-B swizzle): K columns 0-63 / 64-127 and the
+// same for V, from a paged pool [blocks][kv_heads][64][128] bf16 where one
+// CTA walks its (item, head)'s pages (pages of a sequence are consecutive
+// blocks, so one head's pages sit kv_heads * 16 KB apart).
+__global__ void tmap_read(const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv,
+                          int pages_per_cta, int kv_heads, int stages, unsigned long long* sink) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int stage_bytes = 32768;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < stages; ++s)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(full + s)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  const int seq = blockIdx.x / kv_heads, head = blockIdx.x % kv_heads;
+  uint32_t phase[32] = {0};
+  unsigned long long acc = 0;
+  auto issue = [&](int i) {
+    const int s = i % stages;
+    const int row = ((seq * pages_per_cta + i) * kv_heads + head) * 64;
+    uint8_t* st = smem + (size_t)s * stage_bytes;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + s)), "r"(stage_bytes));
+    const CUtensorMap* maps[2] = {&tk, &tv};
+    for (int kv = 0; kv < 2; ++kv)
+      for (int h = 0; h < 2; ++h)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+            " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(su32(st + kv * 16384 + h * 8192)),
+            "l"(maps[kv]), "r"(su32(full + s)), "r"(h * 64), "r"(row), "l"(pol)
+            : "memory");
+  };
+  for (int i = 0; i < stages && i < pages_per_cta; ++i) issue(i);
+  for (int i = 0; i < pages_per_cta; ++i) {
+    const int s = i % stages;
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(su32(full + s)), "r"(phase[s]));
+    phase[s] ^= 1;
+    acc += smem[(size_t)s * stage_bytes];
+    if (i + stages < pages_per_cta) issue(i + stages);
   }
   if (acc == 0xdeadbeef) *sink = acc;
 }
@@ -162,6 +214,42 @@ int main() {
       const double us = ms * 1e3 / reps;
       printf("512MB %4d CTAs x %7zu B (ring %d x %d, smem %d): %6.1f us/launch  %7.1f GB/s\n", c.ctas, per,
              c.stages, c.stage, smem, us, (double)per * c.ctas / (us * 1e-6) / 1e9);
+    }
+  }
+  // the decode attention's access pattern (tensor maps over a paged pool)
+  {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q);
+    const int kv_heads = 8, seqs = 64, pages = 32;  // B=64, ctx 2048, 8 kv heads
+    const uint64_t rows = (uint64_t)seqs * pages * kv_heads * 64;  // pool rows of 256 B
+    const size_t pool_bytes = rows * 256;  // 268 MB each for K and V
+    uint8_t* kbuf = buf;
+    uint8_t* vbuf = buf + pool_bytes;
+    CUtensorMap tk, tv;
+    uint64_t dims[2] = {128, rows};
+    uint64_t strides[1] = {256};
+    uint32_t box[2] = {64, 64};
+    uint32_t es[2] = {1, 1};
+    enc(&tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kbuf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    enc(&tv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, vbuf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    for (int stages : {3, 2}) {
+      const int smem = stages * 32768 + 1024 + 256;
+      cudaFuncSetAttribute(tmap_read, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      for (int w = 0; w < 3; ++w) tmap_read<<<seqs * kv_heads, 32, smem>>>(tk, tv, pages, kv_heads, stages, sink);
+      cudaEventRecord(e0);
+      const int reps = 20;
+      for (int r = 0; r < reps; ++r) tmap_read<<<seqs * kv_heads, 32, smem>>>(tk, tv, pages, kv_heads, stages, sink);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double us = ms * 1e3 / reps;
+      cudaError_t err = cudaGetLastError();
+      printf("paged tmap 512 CTAs x 32 pages x 32 KB (ring %d): %6.1f us/launch  %7.1f GB/s %s\n", stages, us,
+             2.0 * pool_bytes / (us * 1e-6) / 1e9, err == cudaSuccess ? "" : cudaGetErrorString(err));
     }
   }
   for (int tpb : {256, 512, 1024}) {
