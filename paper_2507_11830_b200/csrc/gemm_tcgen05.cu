@@ -1485,11 +1485,17 @@ static int64_t swap_splits(int N, int K, int sms) {
 // variants for 65..256 tokens (tools/swap_probe.py, graph-replayed, gate/up
 // N = 28672 K = 4096 at M = 96 / 128 / 256: 42.2 / 42.6 / 55.2 us tiled vs
 // 46.6 / 48.6 / 62.8 swap-AB; at M <= 64 swap-AB wins, 40.3-41.1 vs 43.0-43.3).
+// Projections with at least one 256-row weight tile per SM (the LM head, 70B
+// gate/up) stay swap-AB only up to 32 tokens, where its two streaming CTAs per
+// SM beat the tiled kernel (graph-replayed, tools/swap_probe.py: 8B LM head
+// M = 1/8/32 182/181/173 -> 157/156/159 us; 70B gate/up M = 1/16 184/151 ->
+// 141/142 us; at M = 64 neutral or worse).
 static bool swap_regime(int M, int N, int sms) {
   using namespace sp::gemm;
   const int64_t n_super = cdiv(N, 256);
-  return M <= 256 && n_super < sms && N % 32 == 0 && (M <= 64 || n_super <= sms / 4) &&
-         getenv("SP_GEMM_NO_SPLITK") == nullptr;
+  if (getenv("SP_GEMM_NO_SPLITK") != nullptr || N % 32 != 0) return false;
+  if (n_super >= sms) return M <= 32;
+  return M <= 256 && (M <= 64 || n_super <= sms / 4);
 }
 
 template <int NT>

@@ -47,7 +47,8 @@ class GemmModel:
     M = 1..4096, graph-replayed): every GEMM costs max(compute, weight
     streaming) plus a fixed, non-overlapped ~9 us; the swap-AB regime
     (M <= 256 token rows, padded to 32; for projections wider than
-    swap_wide_tiles 256-row weight tiles only up to swap_wide_max_rows, as
+    swap_wide_tiles 256-row weight tiles only up to swap_wide_max_rows, with
+    one or more tiles per SM only up to swap_huge_max_rows, as
     gemm_tcgen05.cu:swap_regime) computes at ~800 TFLOP/s, the 128-row tiles
     above it at ~1400."""
 
@@ -56,6 +57,8 @@ class GemmModel:
     swap_max_rows: int = 256
     swap_wide_max_rows: int = 64   # wide projections leave swap-AB above this
     swap_wide_tiles: int = 37      # "wide": more 256-row weight tiles than sms / 4
+    swap_huge_tiles: int = 148     # at least one 256-row weight tile per SM ...
+    swap_huge_max_rows: int = 32   # ... stays swap-AB only up to this many rows
     hbm_gbs: float = 6454.6        # MEASURED_PEAKS.json copy bandwidth
     stream_eff: float = 1.0        # weight streaming, fraction of hbm_gbs
     launch_us: float = 9.0         # per-GEMM fixed cost (launch, fill, drain, tail)
@@ -68,8 +71,11 @@ B200_GEMM = GemmModel()
 def _gemm_us(rows: int, n: int, k: int, g: GemmModel) -> float:
     if rows <= 0:
         return 0.0
-    wide = -(-n // 256) > g.swap_wide_tiles
-    if rows <= (g.swap_wide_max_rows if wide else g.swap_max_rows):
+    tiles = -(-n // 256)
+    wide = tiles > g.swap_wide_tiles
+    limit = g.swap_huge_max_rows if tiles >= g.swap_huge_tiles else (
+        g.swap_wide_max_rows if wide else g.swap_max_rows)
+    if rows <= limit:
         pad, tf = -(-rows // 32) * 32, g.swap_tflops
     else:
         pad, tf = -(-rows // 128) * 128, g.tflops

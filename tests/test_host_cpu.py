@@ -265,7 +265,8 @@ def test_attention_split_plan_covers_every_key_tile_once():
     (1, 4096, 1, 0), (64, 4096, 5, 0), (256, 4096, 2, 0),    # decode: swap-AB (M <= 256)
     (1024, 4096, 2, 1), (8192, 6144, 0, 1),                   # prefill: 2-CTA pairs
     (512, 4096, 2, 128), (512, 6144, 0, 1),                   # wave model at small per-rank M
-    (300, 28672, 3, 1), (1, 128256, 1, 256),                  # SwiGLU forces 256; LM head row
+    (300, 28672, 3, 1), (1, 128256, 1, 0),                    # SwiGLU forces 256; LM head row: swap-AB
+    (32, 57344, 3, 0), (64, 128256, 1, 256),                  # >= 1 weight tile per SM: swap-AB to 32 rows
     (64, 28672, 3, 0), (128, 28672, 3, 256), (256, 6144, 1, 0)])  # wide N leaves swap-AB above 64 rows
 def test_gemm_plan_regimes(M, N, epi, want, monkeypatch):
     """The host-side GEMM plan (sp_gemm_plan, the one function sp_gemm_bf16

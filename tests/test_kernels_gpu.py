@@ -443,6 +443,29 @@ def test_gemm_cta_pair_large_tiles(epi, monkeypatch):
     assert torch.equal(outs["1"], outs["0"])
 
 
+@pytest.mark.parametrize("M", [1, 7, 32])
+def test_gemm_vocab_wide_swap_regime(M):
+    """Projections with at least one 256-row weight tile per SM (the LM head,
+    70B gate/up) run swap-AB up to 32 tokens (items looped per CTA): f32
+    logits and the SwiGLU epilogue match fp32."""
+    from paper_2507_11830_b200 import _lib
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    assert _lib.load().sp_gemm_plan(M, 128256, 1024, ops.EPI_STORE_F32, sms) == 0
+    K = 1024
+    a = rnd(M, K, seed=60)
+    w = rnd(128256, K, seed=61, scale=0.05)
+    d = torch.empty(M, 128256, device="cuda")
+    ops.gemm(a, w, d, ops.EPI_STORE_F32, M=M, N=128256, K=K, lda=K, ldb=K, ldd=128256)
+    assert rel(d, a.float() @ w.float().t()) < 1e-4
+    N = 57344
+    g = rnd(N, K, seed=62, scale=0.05)
+    act = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+    ops.gemm(a, g, act, ops.EPI_SWIGLU, M=M, N=N, K=K, lda=K, ldb=K, ldd=N // 2)
+    v = (a.float() @ g.float().t()).view(M, N // 256, 2, 128)
+    want = (torch.nn.functional.silu(v[:, :, 0]) * v[:, :, 1]).reshape(M, N // 2)
+    assert rel(act, want) < 1e-2
+
+
 @pytest.mark.parametrize("M,ldd", [(1000, 4096), (777, 4352), (8192, 4096)])
 def test_gemm_pair_residual_add_tma_bitexact(M, ldd, monkeypatch):
     """The pair kernel's residual add through TMA boxes (SP_ADD_TMA, default on)
