@@ -120,6 +120,15 @@ def main():
         if layers <= 2 or len(launches) < 40 or "--all" in sys.argv:
             print(f"{L['name'][:34]:34s} {len(L['blocks']):5d} {e0:8.1f} {w0:8.1f} {w1:8.1f} {x0:8.1f} {x1:8.1f}"
                   f" {gap:6.2f} {run:7.1f}")
+            if "--ctas" in sys.argv and len(L["exit"]) > 8:
+                # tail shape: exit-time percentiles, and whether late exits
+                # are the CTAs that entered late (corr of entry vs exit)
+                ex = (np.asarray(L["exit"], dtype=np.float64) - base) / 1e3
+                en = (np.asarray(L["entry"], dtype=np.float64) - base) / 1e3
+                pct = np.percentile(ex, [10, 50, 90])
+                corr = float(np.corrcoef(en, ex)[0, 1]) if en.std() > 0 and ex.std() > 0 else 0.0
+                print(f"{'':34s} entry {en.min():.1f}..{en.max():.1f}  exit p10/p50/p90 "
+                      f"{pct[0]:.1f}/{pct[1]:.1f}/{pct[2]:.1f}  corr(entry, exit) {corr:+.2f}")
         prev_exit = x1
     print("\nper kernel: launches, mean release gap after the predecessor's last exit (us), "
           "mean run from first release to last exit (us), total run")
