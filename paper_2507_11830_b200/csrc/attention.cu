@@ -1211,7 +1211,7 @@ extern "C" sp_status sp_attention(const void* q, int64_t ldq, int64_t q_rows, co
   if (G > 16) return fail(kUnsupported, "attention: GQA group > 16");
   if (ldq % 8 || ldo % 2) return fail(kInvalid, "attention: bad row strides");
   if (block_size <= 0) return fail(kInvalid, "attention: bad block size");
-  attn::Params p;
+  attn::Params p{};
   p.q = static_cast<const __nv_bfloat16*>(q);
   p.ldq = ldq;
   p.k_pool = static_cast<const __nv_bfloat16*>(k_pool);
@@ -1288,7 +1288,7 @@ extern "C" sp_status sp_attention_decode_qkv(
     return fail(kUnsupported, "attention_decode_qkv: block_size must be a multiple of 64");
   if (ld_qkv != (int64_t)(q_heads + 2 * kv_heads) * 128 || ldo % 2)
     return fail(kInvalid, "attention_decode_qkv: ld_qkv must be (q_heads + 2 kv_heads) * 128");
-  attn::Params p;
+  attn::Params p{};
   memset(&p, 0, sizeof(p));
   p.k_pool = static_cast<const __nv_bfloat16*>(k_pool);
   p.v_pool = static_cast<const __nv_bfloat16*>(v_pool);
