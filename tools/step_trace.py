@@ -8,7 +8,8 @@ release, and how much of a launch ran before that release (PDL overlap).
     SP_NVCC_EXTRA=-DSTEP_TRACE python -m paper_2507_11830_b200.build --force
     cp paper_2507_11830_b200/libshiftpar.so paper_2507_11830_b200/libshiftpar_trace.so
     python -m paper_2507_11830_b200.build --force        # production library back
-    python tools/step_trace.py [B] [ctx] [--layers N]    # decode step at batch B
+    python tools/step_trace.py [B] [ctx] [--layers N] [--ctas]   # decode step at batch B
+                                    # (--ctas: per-launch exit percentiles, entry/exit corr)
 """
 import os
 import re
