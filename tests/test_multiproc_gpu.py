@@ -145,18 +145,20 @@ def test_multi_process_engine_matches_loopback(world, sp_degree, fused, monkeypa
         assert fp == repr(want_fp)
 
 
-def test_bench_self_spawns_two_ranks():
-    """`python bench.py --gpus 2` with WORLD_SIZE unset spawns two ranks
+@pytest.mark.parametrize("n", [2, 8])
+def test_bench_self_spawns_ranks(n):
+    """`python bench.py --gpus N` with WORLD_SIZE unset spawns N ranks
     (torch.distributed.run) and rank 0 prints exactly one JSON line carrying
     the SP/TP prefill and decode matrix and the CPU baseline.  Ranks share the
-    one GPU through SP_BENCH_BACKEND=gloo (plumbing check, not a number)."""
+    one GPU through SP_BENCH_BACKEND=gloo (plumbing check, not a number); N=8
+    is the driver's largest scaling point (one kv head per rank at 8B)."""
     import json
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
     env["SP_BENCH_BACKEND"] = "gloo"
-    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", str(n),
                           "--steps", "1", "--warmup", "1", "--seq", "1024", "--layers", "2",
                           "--decode-batch", "4", "--decode-ctx", "256"],
                          env=env, capture_output=True, text=True, timeout=900)
@@ -164,7 +166,7 @@ def test_bench_self_spawns_two_ranks():
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, out.stdout
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["n_gpus"] == n and d["value"] > 0
     m = d["matrix"]
     assert set(m["prefill"]) >= {"sp", "tp"}
     for b in ("b1", "b4"):
