@@ -1044,10 +1044,10 @@ static int decode_tma_splits(int n_items, int kv_heads, int max_kv_len) {
   // B=8 4.03 -> 3.91, B=16 4.57 -> 4.32, B=32 5.28 -> 5.06 vs the old
   // one-wave-of-296 rule.  Tuning override SP_DECODE_SPLITS.
   int want = (256 + ctas - 1) / ctas;
-  if (const char* e = getenv("SP_DECODE_SPLITS")) want = atoi(e);
   const int pages = (max_kv_len + dec::PAGE - 1) / dec::PAGE;
   const int max_useful = ctas < 16 ? (pages + 3) / 4 : (pages / 8 > 1 ? pages / 8 : 1);
   if (want > max_useful) want = max_useful;
+  if (const char* e = getenv("SP_DECODE_SPLITS")) want = atoi(e) < pages ? atoi(e) : pages;
   if (want > 64) want = 64;
   return want < 1 ? 1 : want;
 }
