@@ -1470,12 +1470,14 @@ static int64_t swap_splits(int N, int K, int sms) {
   const int64_t k_blocks = cdiv(K, BK);
   const int64_t n_super = cdiv(N, swp::WT * 128);
   const int64_t slots = (int64_t)sms * T::CTAS_PER_SM;
-  // measured best in-graph: 4/5 of the SMs at one CTA per SM
-  // (tools/decode_ablation.py); ~1.3x the SMs at two per SM (M <= 32,
+  // measured best in-graph: ~1.3x the SMs at two CTAs per SM (M <= 32,
   // tools/gpu_swap_ab.sh: 192 CTAs on 148 SMs beat 148 by 1.0/1.3/0.8% TPOT at
   // B=1/8/32 — more streams in flight, while the N=4096 projections' K splits
-  // stay <= 12, the partial count the consuming norm loads in one batch)
-  int64_t min_ctas = T::CTAS_PER_SM == 2 ? (13 * sms) / 10 : (4 * sms) / 5;
+  // stay <= 12, the partial count the consuming norm loads in one batch); at
+  // one CTA per SM 3/4 of the SMs for NT=64 (tools/gpu_swap64_ab.sh: the
+  // N=4096 projections split 7 ways instead of 8, B=48/64 -0.4/-1.0%) and 4/5
+  // for NT >= 128 (B=128 best at 118-133)
+  int64_t min_ctas = T::CTAS_PER_SM == 2 ? (13 * sms) / 10 : NT <= 64 ? (3 * sms) / 4 : (4 * sms) / 5;
   if (const char* e = getenv("SP_SWAP_MIN_CTAS")) min_ctas = atoi(e);
   int64_t ks = 1;
   while (n_super * ks < min_ctas && ks * 2 <= k_blocks) ++ks;
